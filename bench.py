@@ -1,0 +1,321 @@
+#!/usr/bin/env python3
+"""Bouquets walk-campaign benchmark (BASELINE.json metric "walk steps/sec").
+
+Workload (N=1, BASELINE configs[1]): R-MAT a,b,c = 0.57,0.19,0.19, scale 20,
+edge factor 16, symmetrised/deduplicated/loop-free, largest connected
+component; 16,777,216 walks of length 128 from uniform-random starts, Saba
+(seed-sorted bouquets), uint64 per-vertex visit counts. A "step" of this
+benchmark is one whole campaign; the metric counts walk steps (L-1 per walk),
+as the reference does (walker.hpp:523, bench.hpp:166-168).
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling — N x 16,777,216 walks,
+the flattened (vertex, k) walk list cut into N contiguous ranges (one per
+rank), CSR replicated, one NCCL all-reduce of the int64 counts.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref: the
+reference headers compiled unchanged, OpenMP over all host threads) on a
+bounded sample of the same workload (every 4th start vertex with its full
+walk set), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (generator spec, walks per GPU, length)
+    "cfg2": (("rmat", 20, 16), 1 << 24, 128),
+    "cfg1": (("er", 65536, 524288), 1 << 20, 64),
+}
+BYTES_PER_STEP = 64  # one 32 B sector for {base,deg} + one for adj[base+idx]
+MASTER_SEED = 42
+GRAPH_SEED = 1
+
+
+def make_graph(sb, spec):
+    if spec[0] == "rmat":
+        return sb.make_rmat(spec[1], spec[2], 0.57, 0.19, 0.19, seed=GRAPH_SEED, keep_lcc=True)
+    return sb.make_erdos_renyi(spec[1], spec[2], GRAPH_SEED)
+
+
+def workload_desc(name, g, walks, L):
+    gen = WORKLOADS[name][0]
+    gdesc = (f"R-MAT(0.57,0.19,0.19) scale {gen[1]} ef {gen[2]} LCC" if gen[0] == "rmat"
+             else f"Erdos-Renyi G(n={gen[1]}, m={gen[2]})")
+    return f"{name}: {gdesc} (n={g.n}, m={g.m}); {walks} uniform-start walks x L={L} per GPU"
+
+
+def read_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def read_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = f"/tmp/saba_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 9 and f[1].replace(".", "").isdigit():
+                    rows.append(f)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return int(os.environ.get("RANK", "0")), ws, int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def cpu_reference_run(g, walks, L, stride, threads=0):
+    """The reference's own CPU path on every `stride`-th start vertex."""
+    from oracle.oracle import Reference, reference_available
+    if not reference_available():
+        from oracle.oracle import build
+        build()
+    R = Reference()
+    rg = R.from_csr(g.offsets, g.adjacency)
+    counts, sec, steps = R.campaign_kv(rg, L, W=walks, sorted_=True, lanes=8, threads=threads,
+                                       master=MASTER_SEED, vertex_stride=stride, vertex_phase=0)
+    return steps / sec, sec, steps, R.max_threads() if threads <= 0 else threads
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import paper_2410_14056_b200 as sb
+    spec, walks, L = WORKLOADS[args.workload]
+    g = make_graph(sb, spec)
+    stride = args.cpu_stride
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, sec, steps, cores = cpu_reference_run(g, walks, L, stride)
+        if i >= args.warmup:
+            vals.append((v, sec, steps))
+    value = statistics.median(v for v, _, _ in vals)
+    sample = (f"every {stride}th start vertex of the workload with all its walks "
+              f"({vals[0][2]} steps, {vals[0][1]:.2f} s per sample)")
+    out = {"impl": "reference", "metric": "walk steps/sec (Bouquets)", "value": value,
+           "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": statistics.median(s for _, s, _ in vals) * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+           "data": "synthetic", "config": {"workload": workload_desc(args.workload, g, walks, L),
+                                          "mode": "saba", "lanes": 8},
+           "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "reference",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_14056_b200 as sb
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    spec, walks, L = WORKLOADS[args.workload]
+    mode = sb.WalkMode.Saba if args.mode == "saba" else sb.WalkMode.Hash
+    g = make_graph(sb, spec)
+    cfg = sb.CampaignConfig(length=L, master_seed=MASTER_SEED, mode=mode)
+    total_walks = walks * world
+    steps_per_rank = walks * (L - 1)
+
+    counts = torch.zeros(g.n, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    g.device_handle(local)
+
+    def one_step(timing):
+        counts.zero_()
+        rep = sb.run_walk_campaign_device(g, cfg, counts.data_ptr(), stream.cuda_stream,
+                                          total_walks=total_walks, shard_index=rank,
+                                          shard_count=world, device=local, timing=timing)
+        if world > 1:
+            dist.all_reduce(counts)
+        return rep
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        one_step(False)
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    walk_ms, launches = [], 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            starts[i].record(stream)
+            rep = one_step(True)
+            ends[i].record(stream)
+            walk_ms.append(rep.walk_kernel_ms)
+            launches += rep.launches
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = tot.item() / args.steps
+    value = total_walks * (L - 1) / (ms_per_step * 1e-3)
+
+    # parity spot-check of the last step (cheap, outside timing): total visits
+    total_visits = int(counts.sum().item())
+    assert total_visits == total_walks * L, (total_visits, total_walks * L)
+
+    # end to end through the public API with host buffers (pinned CSR in,
+    # host counts out); every step re-creates the device replica (H2D).
+    pin_off = torch.from_numpy(g.offsets).pin_memory().numpy()
+    pin_adj = torch.from_numpy(g.adjacency).pin_memory().numpy()
+    ge = sb.Graph(pin_off, pin_adj, _trusted=True)
+    e2e_t = []
+    host_counts = torch.zeros(g.n, dtype=torch.int64).pin_memory()
+    for i in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        sink = sb.VisitCountSink(g.n)
+        sb.run_walk_campaign(ge, cfg, sink, total_walks=total_walks, shard_index=rank,
+                             shard_count=world, device=local)
+        if world > 1:
+            ct = torch.from_numpy(sink.counts.view(np.int64)).to(dev)
+            dist.all_reduce(ct)
+            host_counts.copy_(ct)
+        ge.release_device()
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_t.append(t1 - t0)
+    e2e_tot = torch.tensor([sum(e2e_t)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
+    e2e_value = total_walks * (L - 1) / (e2e_tot.item() / args.steps)
+
+    if rank == 0:
+        peak, peak_src = read_peak()
+        kern_ms = statistics.mean(walk_ms)
+        achieved = steps_per_rank * BYTES_PER_STEP / (kern_ms * 1e-3) / 1e9
+        traffic = read_traffic(args.workload)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            v, sec, steps, cores = cpu_reference_run(g, walks, L, args.cpu_stride)
+            cpu = {"value": v, "unit": "steps/s", "cores": cores, "kind": "reference",
+                   "sample": f"oracle/_ref (reference headers, OpenMP) on every {args.cpu_stride}th "
+                             f"start vertex with all its walks: {steps} steps in {sec:.2f} s"}
+        out = {
+            "metric": "walk steps/sec (Bouquets)", "value": value, "unit": "steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": workload_desc(args.workload, g, walks, L),
+                       "mode": args.mode, "lanes": 8, "master_seed": MASTER_SEED,
+                       "graph_seed": GRAPH_SEED, "walks_total": total_walks,
+                       "parallelism": f"walk-range shards x{world}, CSR replicated, NCCL all-reduce",
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "walk_count_kernel (K2)", "kernel_ms": kern_ms,
+                         "step_share": kern_ms / ms_per_step,
+                         "bytes_per_step": BYTES_PER_STEP, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "steps/s",
+                    "h2d_bytes_per_step": int(g.offsets.nbytes + g.adjacency.nbytes),
+                    "d2h_bytes_per_step": int(g.n * 8)},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="saba", choices=["saba", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--mode", default="saba", choices=["saba", "hash"])
+    ap.add_argument("--cpu-stride", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,332 @@
+// Bouquets walk campaigns on sm_100a.
+//
+//   K1a start_hist_kernel   uniform-random starts: K_v histogram
+//   K1b CUB scan            K_v -> walk-list offsets
+//   K1c gen_keys_kernel     per-vertex walk seeds counter_hash(vseed,k)>>32
+//                           (walker.hpp:437-438) as keys (v<<32 | seed), plus
+//                           the step-0 visit of every walk (walker.hpp:216-220)
+//   K1d CUB segmented sort  SABA: seeds sorted within each start vertex
+//                           (walker.hpp:439) -> a warp is a 32-lane bouquet
+//   K2  walk_count_kernel   L-1 lockstep hashed steps per lane
+//                           (walker.hpp:221-235) + VisitCountSink epilogue
+//                           (walker.hpp:355) as warp-aggregated L2 reductions
+//
+// A GPU bouquet is a warp: lanes hold consecutive entries of the sorted key
+// array, so they share their start vertex and hold adjacent seeds — the
+// reference's lane-batched bouquet (walker.hpp:207-236) at width 32. Each
+// thread advances WPT independent bouquet lanes so that several dependent
+// gather chains are in flight per thread (the walk is a pure random-gather
+// workload: no tensor cores).
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
+
+#include <algorithm>
+#include <chrono>
+
+#include "device_graph.cuh"
+#include "saba_hash.cuh"
+#include "walk_common.cuh"
+
+namespace saba_cu {
+
+namespace {
+
+constexpr int kWalkThreads = 256;
+
+__global__ void start_hist_kernel(uint64_t W, uint64_t start_stream, uint32_t n,
+                                  uint32_t* __restrict__ kv) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < W; w += stride) {
+        const uint32_t v = scaled_index(uint32_t(counter_hash(start_stream, w) >> 32), n);
+        atomicAdd(kv + v, 1u);
+    }
+}
+
+struct U32ToU64 {
+    __host__ __device__ uint64_t operator()(uint32_t x) const { return x; }
+};
+
+// Warp per start vertex. The walk list of this call is [r0, r1) of the
+// flattened (vertex, k) list; keys land at [0, r1 - r0).
+__global__ void gen_keys_kernel(uint32_t n, const uint32_t* __restrict__ kv, uint64_t k_uniform,
+                                const uint64_t* __restrict__ off, uint64_t r0, uint64_t r1,
+                                uint64_t master, uint64_t* __restrict__ keys,
+                                int* __restrict__ seg, unsigned long long* __restrict__ counts) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t v = warp; v < n; v += nwarps) {
+        const uint64_t K = kv ? kv[v] : k_uniform;
+        const uint64_t o = kv ? off[v] : uint64_t(v) * k_uniform;
+        const uint64_t lo = o > r0 ? o : r0;
+        const uint64_t hi = (o + K) < r1 ? (o + K) : r1;
+        if (lane == 0) {
+            const uint64_t b = lo < r1 ? lo : r1;
+            seg[v] = int(b - r0);
+            if (v == n - 1) seg[n] = int(r1 - r0);
+            if (hi > lo) counts[v] += hi - lo;  // step-0 visits; this warp owns v
+        }
+        if (hi <= lo) continue;
+        const uint64_t vseed = substream(master, v);
+        for (uint64_t k = lo - o + lane; k < hi - o; k += 32)
+            keys[o + k - r0] = (uint64_t(v) << 32) | walk_seed(vseed, k);
+    }
+}
+
+template <int WPT>
+__global__ void __launch_bounds__(kWalkThreads)
+    walk_count_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                      const uint64_t* __restrict__ keys, uint64_t nwalks, uint32_t L, uint64_t mult,
+                      unsigned long long* __restrict__ counts) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t base = warp * 32 * WPT; base < nwalks; base += nwarps * 32 * WPT) {
+        uint32_t cur[WPT], seed[WPT];
+        bool act[WPT];
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {
+            const uint64_t i = base + uint64_t(r) * 32 + lane;
+            act[r] = i < nwalks;
+            const uint64_t k = act[r] ? __ldcs(reinterpret_cast<const unsigned long long*>(keys) + i) : 0;
+            cur[r] = uint32_t(k >> 32);
+            seed[r] = uint32_t(k);
+        }
+        for (uint32_t l = 1; l < L; ++l) {
+            uint2 rec[WPT];
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) rec[r] = act[r] ? ldg_csr(csr + cur[r]) : make_uint2(0, 0);
+            uint32_t nxt[WPT];
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) {
+                const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
+                nxt[r] = act[r] ? ldg_u32(adj + rec[r].x + scaled_index(raw, rec[r].y)) : 0u;
+            }
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) {
+                cur[r] = nxt[r];
+                warp_count_visit(counts, nxt[r], act[r], lane);
+            }
+        }
+    }
+}
+
+// One thread per walk; materialises the path (random_walk, walker.hpp:283-302).
+__global__ void walk_paths_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                                  const uint32_t* __restrict__ starts,
+                                  const uint32_t* __restrict__ seeds, uint64_t count, uint32_t L,
+                                  uint64_t mult, uint32_t* __restrict__ paths) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+        uint32_t cur = starts[i];
+        const uint32_t seed = seeds[i];
+        uint32_t* out = paths + i * L;
+        out[0] = cur;
+        for (uint32_t l = 1; l < L; ++l) {
+            const uint2 rec = ldg_csr(csr + cur);
+            cur = ldg_u32(adj + rec.x + scaled_index(seed ^ hash_state(mult, cur, l), rec.y));
+            out[l] = cur;
+        }
+    }
+}
+
+constexpr int kWalksPerThread = 4;
+constexpr uint64_t kChunkWalks = uint64_t(1) << 27;  // keys per pass (1 GiB x2)
+
+int walk_grid(saba_cu_graph* g) {
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &blocks_per_sm, walk_count_kernel<kWalksPerThread>, kWalkThreads, 0));
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    return g->sm_count * blocks_per_sm;
+}
+
+void validate_campaign(const saba_cu_graph* g, const saba_cu_campaign_config& c) {
+    // walker.hpp:461-468, same order and messages
+    if (c.total_walks == 0) check_arg(c.walks_per_vertex >= 1, "walks_per_vertex must be >= 1");
+    check_arg(c.length >= 1, "length must be >= 1");
+    check_arg(c.lanes >= 1 && c.lanes <= 64 && (c.lanes & (c.lanes - 1)) == 0,
+              "lanes must be a power of two in [1, 64]");
+    if (c.length > 1)
+        check_arg(g->min_degree >= 1, "campaign requires degree >= 1 at every vertex when L > 1");
+    check_arg(c.mode == SABA_MODE_HASH || c.mode == SABA_MODE_SABA,
+              "mode not supported on GPU (naive/vector-mod are CPU LCG baselines)");
+    check_arg(c.shard_count >= 1 && c.shard_index < c.shard_count, "bad shard index/count");
+}
+
+
+// Enqueue the whole campaign shard on `st`. Returns walks executed.
+uint64_t enqueue_campaign(saba_cu_graph* g, const saba_cu_campaign_config& c,
+                          unsigned long long* counts, cudaStream_t st, bool timing,
+                          float* walk_ms, uint32_t* launches) {
+    const uint32_t n = g->n;
+    const bool uniform_starts = c.total_walks > 0;
+    const uint64_t total = uniform_starts ? c.total_walks : uint64_t(n) * c.walks_per_vertex;
+    check_arg(uniform_starts || c.walks_per_vertex <= (uint64_t(1) << 40) / (n ? n : 1),
+              "walks_per_vertex too large");
+    const uint64_t r0 = total * c.shard_index / c.shard_count;
+    const uint64_t r1 = total * (uint64_t(c.shard_index) + 1) / c.shard_count;
+    uint32_t* kv = nullptr;
+    uint64_t* off = nullptr;
+    if (uniform_starts) {
+        kv = static_cast<uint32_t*>(g->kv.ensure(sizeof(uint32_t) * n));
+        off = static_cast<uint64_t*>(g->off.ensure(sizeof(uint64_t) * (size_t(n) + 1)));
+        SABA_CUDA_CHECK(cudaMemsetAsync(kv, 0, sizeof(uint32_t) * n, st));
+        const uint64_t sstream = substream(c.master_seed, kStartTag);
+        const int hb = int(std::min<uint64_t>((c.total_walks + 255) / 256, uint64_t(g->sm_count) * 16));
+        start_hist_kernel<<<hb, 256, 0, st>>>(c.total_walks, sstream, n, kv);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        ++*launches;
+        size_t tmp = 0;
+        cub::TransformInputIterator<uint64_t, U32ToU64, const uint32_t*> it(kv, U32ToU64());
+        SABA_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, it, off, int(n), st));
+        void* t = g->cub_tmp.ensure(tmp);
+        SABA_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t, tmp, it, off, int(n), st));
+        ++*launches;
+    }
+    const uint64_t chunk_cap = std::min<uint64_t>(kChunkWalks, r1 - r0 ? r1 - r0 : 1);
+    uint64_t* keys = static_cast<uint64_t*>(g->keys.ensure(sizeof(uint64_t) * chunk_cap));
+    uint64_t* keys_alt = c.mode == SABA_MODE_SABA
+                             ? static_cast<uint64_t*>(g->keys_alt.ensure(sizeof(uint64_t) * chunk_cap))
+                             : nullptr;
+    int* seg = static_cast<int*>(g->seg.ensure(sizeof(int) * (size_t(n) + 1)));
+    const int walk_blocks = walk_grid(g);
+    float total_walk_ms = 0.f;
+    for (uint64_t a = r0; a < r1; a += chunk_cap) {
+        const uint64_t b = std::min(r1, a + chunk_cap);
+        const uint64_t nw = b - a;
+        const int gb = int(std::min<uint64_t>((uint64_t(n) * 32 + 255) / 256, uint64_t(g->sm_count) * 32));
+        gen_keys_kernel<<<gb, 256, 0, st>>>(n, kv, c.walks_per_vertex, off, a, b, c.master_seed, keys,
+                                            seg, counts);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        ++*launches;
+        const uint64_t* walk_keys = keys;
+        if (c.mode == SABA_MODE_SABA) {
+            size_t tmp = 0;
+            SABA_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, keys, keys_alt, int(nw),
+                                                               int(n), seg, seg + 1, st));
+            void* t = g->cub_tmp.ensure(tmp);
+            SABA_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(t, tmp, keys, keys_alt, int(nw), int(n),
+                                                               seg, seg + 1, st));
+            ++*launches;
+            walk_keys = keys_alt;
+        }
+        if (c.length > 1) {
+            if (timing) SABA_CUDA_CHECK(cudaEventRecord(g->ev1, st));
+            walk_count_kernel<kWalksPerThread><<<walk_blocks, kWalkThreads, 0, st>>>(
+                g->d_csr, g->d_adj, walk_keys, nw, c.length, c.hash_multiplier, counts);
+            SABA_CUDA_CHECK(cudaGetLastError());
+            ++*launches;
+            if (timing) {
+                SABA_CUDA_CHECK(cudaEventRecord(g->ev2, st));
+                SABA_CUDA_CHECK(cudaEventSynchronize(g->ev2));
+                float ms = 0.f;
+                SABA_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev1, g->ev2));
+                total_walk_ms += ms;
+            }
+        }
+    }
+    if (walk_ms) *walk_ms = total_walk_ms;
+    return r1 - r0;
+}
+
+void fill_report(const saba_cu_graph* g, const saba_cu_campaign_config& c, uint64_t shard_walks,
+                 saba_cu_campaign_report* rep) {
+    const uint64_t total = c.total_walks > 0 ? c.total_walks : uint64_t(g->n) * c.walks_per_vertex;
+    rep->total_steps = total * (c.length - 1);
+    rep->total_events = total * c.length;
+    rep->shard_walks = shard_walks;
+    rep->shard_steps = shard_walks * (c.length - 1);
+}
+
+}  // namespace
+}  // namespace saba_cu
+
+using namespace saba_cu;
+
+extern "C" {
+
+int saba_cu_walk_paths(saba_cu_graph* g, const uint32_t* starts, const uint32_t* seeds,
+                       uint64_t count, uint32_t length, uint64_t mult, uint32_t* paths_out) {
+    return guard([&] {
+        check_arg(g && (count == 0 || (starts && seeds && paths_out)), "null argument");
+        check_arg(length >= 1, "walk length must be >= 1");  // walker.hpp:271
+        for (uint64_t i = 0; i < count; ++i) {
+            check_arg(starts[i] < g->n, "start vertex out of range");
+            check_arg(length == 1 || g->h_off[starts[i] + 1] > g->h_off[starts[i]],
+                      "cannot walk from an isolated vertex");
+        }
+        if (count == 0) return;
+        DeviceScope scope(g->device);
+        DevBuf d_st, d_sd, d_p;
+        d_st.ensure(sizeof(uint32_t) * count);
+        d_sd.ensure(sizeof(uint32_t) * count);
+        d_p.ensure(sizeof(uint32_t) * count * length);
+        SABA_CUDA_CHECK(cudaMemcpy(d_st.p, starts, sizeof(uint32_t) * count, cudaMemcpyHostToDevice));
+        SABA_CUDA_CHECK(cudaMemcpy(d_sd.p, seeds, sizeof(uint32_t) * count, cudaMemcpyHostToDevice));
+        const int blocks = int(std::min<uint64_t>((count + 255) / 256, uint64_t(g->sm_count) * 8));
+        walk_paths_kernel<<<blocks, 256>>>(g->d_csr, g->d_adj, d_st.as<uint32_t>(), d_sd.as<uint32_t>(),
+                                           count, length, mult, d_p.as<uint32_t>());
+        SABA_CUDA_CHECK(cudaGetLastError());
+        SABA_CUDA_CHECK(cudaMemcpy(paths_out, d_p.p, sizeof(uint32_t) * count * length,
+                                   cudaMemcpyDeviceToHost));
+    });
+}
+
+int saba_cu_walk_campaign_device(saba_cu_graph* g, const saba_cu_campaign_config* cfg,
+                                 uint64_t* counts_dev, void* stream, int timing,
+                                 saba_cu_campaign_report* rep) {
+    return guard([&] {
+        check_arg(g && cfg && counts_dev, "null argument");
+        validate_campaign(g, *cfg);
+        DeviceScope scope(g->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        saba_cu_campaign_report r{};
+        float walk_ms = 0.f;
+        if (timing) SABA_CUDA_CHECK(cudaEventRecord(g->ev0, st));
+        const uint64_t w = enqueue_campaign(g, *cfg, reinterpret_cast<unsigned long long*>(counts_dev),
+                                            st, timing != 0, &walk_ms, &r.launches);
+        if (timing) {
+            SABA_CUDA_CHECK(cudaEventRecord(g->ev1, st));
+            SABA_CUDA_CHECK(cudaEventSynchronize(g->ev1));
+            float ms = 0.f;
+            SABA_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+            r.seconds = ms * 1e-3;
+            r.walk_kernel_ms = walk_ms;
+        }
+        fill_report(g, *cfg, w, &r);
+        if (rep) *rep = r;
+    });
+}
+
+int saba_cu_walk_campaign(saba_cu_graph* g, const saba_cu_campaign_config* cfg,
+                          uint64_t* counts_out, saba_cu_campaign_report* rep) {
+    return guard([&] {
+        check_arg(g && cfg && counts_out, "null argument");
+        validate_campaign(g, *cfg);
+        DeviceScope scope(g->device);
+        DevBuf d_counts;
+        d_counts.ensure(sizeof(uint64_t) * g->n);
+        SABA_CUDA_CHECK(cudaMemsetAsync(d_counts.p, 0, sizeof(uint64_t) * g->n, 0));
+        saba_cu_campaign_report r{};
+        float walk_ms = 0.f;
+        SABA_CUDA_CHECK(cudaEventRecord(g->ev0, 0));
+        const uint64_t w = enqueue_campaign(g, *cfg, d_counts.as<unsigned long long>(), 0, true,
+                                            &walk_ms, &r.launches);
+        SABA_CUDA_CHECK(cudaEventRecord(g->ev1, 0));
+        SABA_CUDA_CHECK(cudaEventSynchronize(g->ev1));
+        float ms = 0.f;
+        SABA_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+        r.seconds = ms * 1e-3;
+        r.walk_kernel_ms = walk_ms;
+        SABA_CUDA_CHECK(cudaMemcpy(counts_out, d_counts.p, sizeof(uint64_t) * g->n,
+                                   cudaMemcpyDeviceToHost));
+        fill_report(g, *cfg, w, &r);
+        if (rep) *rep = r;
+    });
+}
+
+}  // extern "C"

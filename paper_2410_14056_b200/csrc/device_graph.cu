@@ -1,0 +1,149 @@
+// K0: device CSR upload and the handle lifecycle; library identification.
+#include <cstring>
+#include <string>
+
+#include "device_graph.cuh"
+#include "saba_hash.cuh"
+
+namespace saba_cu {
+
+namespace {
+thread_local std::string t_last_error;
+
+// off[v], off[v+1] -> packed {base, degree}: the two values every step reads
+// together (walker.hpp:225-226) become one 8-byte gather.
+__global__ void pack_csr_kernel(const uint32_t* __restrict__ off, uint32_t n, uint2* __restrict__ csr) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint32_t b = off[v];
+        csr[v] = make_uint2(b, off[v + 1] - b);
+    }
+}
+}  // namespace
+
+void set_last_error(const std::string& msg) { t_last_error = msg; }
+
+void release_aesc_state(saba_cu_graph* g);  // aesc.cu
+
+const std::vector<uint32_t>& slot_edges(saba_cu_graph* g) {
+    if (!g->h_slot_edge.empty() || g->m == 0) return g->h_slot_edge;
+    // edge ids are ranks of the (u<v) pairs in sorted order (graph.hpp:92-100)
+    const auto& off = g->h_off;
+    const auto& adj = g->h_adj;
+    std::vector<uint32_t> se(2 * g->m);
+    uint32_t e = 0;
+    for (uint32_t u = 0; u < g->n; ++u)
+        for (uint32_t s = off[u]; s < off[u + 1]; ++s)
+            if (adj[s] > u) se[s] = e++;
+    for (uint32_t u = 0; u < g->n; ++u)
+        for (uint32_t s = off[u]; s < off[u + 1]; ++s)
+            if (adj[s] < u) {
+                const uint32_t v = adj[s];
+                uint32_t lo = off[v], hi = off[v + 1];
+                while (lo < hi) {
+                    const uint32_t mid = lo + (hi - lo) / 2;
+                    if (adj[mid] < u) lo = mid + 1; else hi = mid;
+                }
+                se[s] = se[lo];
+            }
+    g->h_slot_edge.swap(se);
+    return g->h_slot_edge;
+}
+
+}  // namespace saba_cu
+
+saba_cu_graph::~saba_cu_graph() {
+    saba_cu::release_aesc_state(this);
+    if (d_csr) cudaFree(d_csr);
+    if (d_adj) cudaFree(d_adj);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (ev2) cudaEventDestroy(ev2);
+}
+
+using namespace saba_cu;
+
+extern "C" {
+
+const char* saba_cu_last_error(void) { return t_last_error.c_str(); }
+
+const char* saba_cu_version(void) { return "saba_cuda 0.1 sm_100a"; }
+
+int saba_cu_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uint32_t n,
+                         uint64_t two_m, int device, saba_cu_graph** out) {
+    return guard([&] {
+        check_arg(out != nullptr && offsets != nullptr, "null argument");
+        check_arg(two_m == 0 || adjacency != nullptr, "null adjacency");
+        check_data(n > 0, "empty graph");
+        check_data(offsets[0] == 0 && offsets[n] == two_m && two_m % 2 == 0,
+                   "offsets do not describe a 2m-slot adjacency");
+        check_data(two_m <= 0xffffffffull, "graph too large: 2m must fit in 32 bits");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            throw CudaError("no CUDA device available (libsaba_cuda has no CPU fallback)");
+        }
+        check_arg(device >= 0 && device < ndev, "device index out of range");
+        DeviceScope scope(device);
+        cudaDeviceProp prop;
+        SABA_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+        check_data(prop.major >= 10, "libsaba_cuda is built for sm_100a (B200)");
+
+        auto g = std::make_unique<saba_cu_graph>();
+        g->device = device;
+        g->sm_count = prop.multiProcessorCount;
+        g->n = n;
+        g->m = two_m / 2;
+        g->h_off.assign(offsets, offsets + n + 1);
+        g->h_adj.assign(adjacency, adjacency + two_m);
+        uint32_t dmin = UINT32_MAX, dmax = 0;
+        for (uint32_t v = 0; v < n; ++v) {
+            check_data(offsets[v] <= offsets[v + 1], "offsets must be nondecreasing");
+            const uint32_t d = offsets[v + 1] - offsets[v];
+            dmin = d < dmin ? d : dmin;
+            dmax = d > dmax ? d : dmax;
+        }
+        for (uint64_t s = 0; s < two_m; ++s) check_data(adjacency[s] < n, "adjacency id out of range");
+        g->min_degree = dmin;
+        g->max_degree = dmax;
+
+        uint32_t* d_off = nullptr;
+        SABA_CUDA_CHECK(cudaMalloc(&d_off, sizeof(uint32_t) * (size_t(n) + 1)));
+        SABA_CUDA_CHECK(cudaMalloc(&g->d_csr, sizeof(uint2) * size_t(n)));
+        SABA_CUDA_CHECK(cudaMalloc(&g->d_adj, sizeof(uint32_t) * (two_m ? two_m : 1)));
+        SABA_CUDA_CHECK(cudaMemcpy(d_off, offsets, sizeof(uint32_t) * (size_t(n) + 1),
+                                   cudaMemcpyHostToDevice));
+        if (two_m)
+            SABA_CUDA_CHECK(cudaMemcpy(g->d_adj, adjacency, sizeof(uint32_t) * two_m,
+                                       cudaMemcpyHostToDevice));
+        pack_csr_kernel<<<(n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096, 256>>>(d_off, n, g->d_csr);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        SABA_CUDA_CHECK(cudaDeviceSynchronize());
+        cudaFree(d_off);
+        SABA_CUDA_CHECK(cudaEventCreate(&g->ev0));
+        SABA_CUDA_CHECK(cudaEventCreate(&g->ev1));
+        SABA_CUDA_CHECK(cudaEventCreate(&g->ev2));
+        *out = g.release();
+    });
+}
+
+int saba_cu_graph_destroy(saba_cu_graph* g) {
+    return guard([&] {
+        if (!g) return;
+        DeviceScope scope(g->device);
+        delete g;
+    });
+}
+
+uint32_t saba_cu_graph_vertex_count(const saba_cu_graph* g) { return g ? g->n : 0; }
+uint64_t saba_cu_graph_edge_count(const saba_cu_graph* g) { return g ? g->m : 0; }
+
+}  // extern "C"

@@ -1,0 +1,32 @@
+// Device helpers shared by the campaign (K2) and AESC walk-phase (K4) kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace saba_cu {
+
+// One 8-byte read-only gather of {base, degree} (LDG.E.64.CONSTANT).
+__device__ __forceinline__ uint2 ldg_csr(const uint2* p) { return __ldg(p); }
+__device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
+
+// VisitCountSink epilogue (walker.hpp:355) with warp aggregation: lanes of a
+// SABA bouquet sit on the same vertex in runs of adjacent lanes, so the head
+// of every run of equal `v` (found with one shuffle + ballot) issues a single
+// L2 reduction for the whole run. Divergent lanes degrade to one reduction
+// each. Active lanes must form a prefix of the warp; all 32 lanes must call.
+__device__ __forceinline__ void warp_count_visit(unsigned long long* __restrict__ counts, uint32_t v,
+                                                 bool act, uint32_t lane) {
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
+    const uint32_t amask = __ballot_sync(0xffffffffu, act);
+    const bool head = act && (lane == 0 || prev != v);
+    const uint32_t heads = __ballot_sync(0xffffffffu, head);
+    if (head) {
+        const uint32_t later = heads & ~((2u << lane) - 1u);  // heads strictly above lane
+        const uint32_t end = later ? uint32_t(__ffs(later) - 1) : uint32_t(__popc(amask));
+        atomicAdd(counts + v, static_cast<unsigned long long>(end - lane));
+    }
+}
+
+}  // namespace saba_cu

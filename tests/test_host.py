@@ -1,0 +1,146 @@
+"""CPU-only checks of the product's host side: the C ABI loads and exports
+every symbol include/saba_cuda.h declares; host graph construction matches the
+reference's canonical CSR; generators are deterministic and well-formed;
+host-side integer primitives match the oracle; no CPU fallback exists."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden_graph
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "saba_cuda.h")).read()
+    return sorted(set(re.findall(r"SABA_API\s+[\w\s\*]+?\b(saba_\w+)\(", src)))
+
+
+def test_header_symbols_exported(sb):
+    import ctypes
+
+    import paper_2410_14056_b200._lib as L
+    syms = header_symbols()
+    assert len(syms) >= 25
+    so = ctypes.CDLL(L.LIB_PATH)
+    for s in syms:
+        assert hasattr(so, s), s
+    assert set(syms) == set(L.SIGNATURES), set(syms) ^ set(L.SIGNATURES)
+    assert L.lib().saba_cu_version().decode().startswith("saba_cuda")
+
+
+def test_no_cpu_fallback(sb, gpu_available):
+    if gpu_available:
+        pytest.skip("GPU present: fallback check only meaningful without a device")
+    g = sb.triangle()
+    with pytest.raises(sb.CudaError):
+        sb.random_walk(g, 0, 3, sb.SelectorKind.Scaled, 1)
+    with pytest.raises(sb.CudaError):
+        sb.run_walk_campaign(g, sb.CampaignConfig(walks_per_vertex=1, length=2), sb.VisitCountSink(3))
+
+
+def test_named_graph_csr_matches_reference(golden, sb):
+    ctor = {"triangle": sb.triangle, "fig1": sb.fig1, "grid3x3": sb.grid3x3,
+            "petersen": sb.petersen, "P5": lambda: sb.path(5), "P100": lambda: sb.path(100),
+            "S5": lambda: sb.star(5), "K4": lambda: sb.complete(4), "K20": lambda: sb.complete(20)}
+    for name, f in ctor.items():
+        g = f()
+        assert np.array_equal(g.offsets, golden[f"g/{name}/off"]), name
+        assert np.array_equal(g.adjacency, golden[f"g/{name}/adj"]), name
+        assert np.array_equal(g.slot_edges(), golden[f"g/{name}/slot_edge"]), name
+
+
+def test_reference_generators_reproduced(golden, sb):
+    for name, g in (("sf300_4_5", sb.make_scale_free(300, 4, 5)),
+                    ("sf400_5_21", sb.make_scale_free(400, 5, 21)),
+                    ("sf2000_8_17", sb.make_scale_free(2000, 8, 17)),
+                    ("rc120_150_31", sb.make_random_connected(120, 150, 31)),
+                    ("rc40_30_13", sb.make_random_connected(40, 30, 13))):
+        assert np.array_equal(g.offsets, golden[f"g/{name}/off"]), name
+        assert np.array_equal(g.adjacency, golden[f"g/{name}/adj"]), name
+
+
+def test_from_edges_canonicalises(sb):
+    g = sb.Graph.from_edges(2, [(0, 1), (1, 0), (0, 0)])  # test_graph.cpp:31-35
+    assert g.n == 2 and g.m == 1
+    g = sb.Graph.from_edges(5, [(4, 0), (0, 4), (2, 1), (3, 3)])
+    assert g.n == 5 and g.m == 2 and list(g.neighbors(0)) == [4]
+    with pytest.raises(RuntimeError):
+        sb.Graph.from_edges(0, [])
+    with pytest.raises(RuntimeError):  # unsorted slice rejected
+        sb.Graph(np.array([0, 2, 3, 4], np.uint32), np.array([2, 1, 0, 0], np.uint32))
+
+
+def _check_csr(g):
+    off, adj = g.offsets, g.adjacency
+    deg = np.diff(off)
+    u = np.repeat(np.arange(g.n), deg)
+    assert (adj != u).all()
+    # sorted strictly increasing within each slice
+    inner = np.ones(len(adj), bool)
+    inner[off[:-1][deg > 0]] = False
+    assert (np.diff(adj.astype(np.int64))[inner[1:]] > 0).all()
+    # symmetric
+    a = set(zip(u.tolist(), adj.tolist()))
+    assert all((v, w) in a for (w, v) in list(a)[:5000])
+
+
+def test_erdos_renyi(sb):
+    g = sb.make_erdos_renyi(4096, 32768, 3)
+    assert g.n == 4096 and g.m == 32768
+    _check_csr(g)
+    g2 = sb.make_erdos_renyi(4096, 32768, 3)
+    assert np.array_equal(g.adjacency, g2.adjacency)
+    assert not np.array_equal(g.adjacency, sb.make_erdos_renyi(4096, 32768, 4).adjacency)
+
+
+def test_rmat_lcc(sb, oracle):
+    g = sb.make_rmat(12, 8, seed=5)
+    _check_csr(g)
+    assert oracle.is_connected(g.offsets, g.adjacency)
+    assert g.degrees().min() >= 1
+    assert np.array_equal(g.adjacency, sb.make_rmat(12, 8, seed=5).adjacency)
+    raw = sb.make_rmat(12, 8, seed=5, keep_lcc=False)
+    assert raw.n == 4096 and raw.m >= g.m
+    lcc = sb.largest_component(raw)
+    assert np.array_equal(lcc.offsets, g.offsets) and np.array_equal(lcc.adjacency, g.adjacency)
+
+
+def test_chung_lu(sb, oracle):
+    g = sb.make_chung_lu(20000, 2.2, 20.0, 500.0, seed=3)
+    _check_csr(g)
+    assert oracle.is_connected(g.offsets, g.adjacency)
+    assert g.max_degree() <= 700
+    assert 6.0 < 2 * g.m / g.n < 30.0
+
+
+def test_host_primitives_match_oracle(sb, oracle):
+    rng = np.random.default_rng(1)
+    xs = rng.integers(0, 2**63, 200, dtype=np.uint64)
+    for x in xs[:50]:
+        assert int(sb.mix64(x)) == oracle.mix64(int(x))
+        assert int(sb.counter_hash(x, 17)) == oracle.counter_hash(int(x), 17)
+        assert int(sb.substream(x, 5)) == oracle.substream(int(x), 5)
+        v, l = int(x) & 0xFFFFFFFF, int(x) >> 40
+        assert int(sb.hash_state(v, l)) == oracle.hash_state(v, l)
+    assert np.array_equal(sb.uniform_start_counts(777, 50000, 9),
+                          oracle.uniform_start_counts(777, 50000, 9))
+
+
+def test_seed_sets(sb):
+    s = sb.gen_sorted_seeds(10000, 0x5EED)  # test_rng.cpp:444-461
+    assert (np.diff(s.seeds.astype(np.int64)) >= 0).all()
+    u = sb.gen_seeds(10000, 0x5EED, sb.SeedOrdering.AsGenerated)
+    assert np.array_equal(np.sort(u.seeds), s.seeds)
+    with pytest.raises(ValueError):
+        sb.gen_sorted_seeds(0, 1)
+
+
+def test_walk_budget_host(sb, golden):
+    assert sb.walk_budget(5, 0.05, 0.05, 4, 100) == 44936
+    for t, eps, delta, d, m, want in golden["walk_budget"]:
+        assert sb.walk_budget(int(t), eps, delta, int(d), int(m)) == int(want)
+    with pytest.raises(ValueError):
+        sb.walk_budget(0, 0.05, 0.05, 1, 10)
+    with pytest.raises(ValueError):
+        sb.walk_budget(1, 0.0, 0.05, 1, 10)
