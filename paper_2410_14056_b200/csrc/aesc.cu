@@ -1,13 +1,698 @@
-// TGT+ AESC on sm_100a (placeholder until the estimator kernels land).
+// TGT+ all-edges spanning centrality (aesc.hpp) on sm_100a.
+//
+// Per batch of up to S = 64 sources (one float64 column each):
+//   K3a aesc_init      depth-0 state: p_0 = e_src, g_hat = 1/d_i + bip
+//                      (aesc.hpp:577, 290-301)
+//   K3b aesc_check     per-source crossover test of advance_to_switch
+//                      (aesc.hpp:391-394): l < tau_src, cap, and
+//                      support_degree_sum >= source_budget_sum(l) with the
+//                      reference's repeated-addition budget (exact fallback
+//                      whenever the fast bound cannot decide), freezing
+//                      the source at tau~ = l
+//   K3c aesc_rho       rho = p_tau~ * inv_deg for frozen sources (aesc.hpp:597-602)
+//   K3d aesc_expand    sparse frontier: candidate rows of depth l+1
+//   K3e aesc_pull      p_{l+1}(x) = sum_{v in N(x)} p_l(v)/d(v) for all 64
+//                      columns at once (row = 512 B, lane = 2 columns), the
+//                      support masks (support(l+1) = N(support(l)),
+//                      aesc.hpp:313-325) and the exact support degree sums
+//   K3f aesc_hook      g_hat[s] += p_l(i)/d_i - p_l(j)/d_j (aesc.hpp:581-588)
+//   K4  aesc_walk      two-way walk pairs (aesc.hpp:448-525): a block owns a
+//                      tile of 2048 pair indices, sorts each side's seeds in
+//                      shared memory (a SABA bouquet per warp, PAPER Alg. 3),
+//                      walks them scoring rho in step order, and reduces
+//                      (a_k - b_k) / n_req with a fixed tree
+//   K4b aesc_slot_reduce  per directed slot: tile partials folded in tile
+//                      order, g_hat[s] += acc (aesc.hpp:624)
+//   K5  aesc_symmetrise s_hat[e] = g_hat[u->v] + g_hat[v->u] (aesc.hpp:702-706)
+//
+// Exactness: tau, tau~ and n_req are integers decided exactly as the
+// reference decides them (host plan restated bit-for-bit; the support degree
+// sums are exact integers; budgets use the same float64 operations). The
+// float64 values differ from the reference only by summation order (pull in
+// ascending-neighbour order vs push in discovery order; tree vs left fold),
+// far inside the 1e-9 relative contract. Every column's arithmetic is
+// independent of which other sources share its batch (rows outside a
+// column's support hold exact +0.0) and of the GPU count, so results are
+// run-to-run and shard-count invariant.
+//
+// Buffer invariant: outside the rows a batch touches, P/Q/M/R are all zero.
+// Double buffering keeps it within a batch (support(l+2) contains
+// support(l)), and aesc_clear restores it between batches.
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <vector>
+
 #include "device_graph.cuh"
 #include "plan_host.hpp"
+#include "saba_hash.cuh"
+#include "walk_common.cuh"
 
 namespace saba_cu {
-struct AescState {};
+
+constexpr int kCols = 64;           // sources per propagation batch
+constexpr int kTileThreads = 256;   // walk-phase block
+constexpr int kTileIPT = 8;         // walks per thread per side
+constexpr int kTile = kTileThreads * kTileIPT;  // pair indices per tile
+
+struct AescState {
+    uint32_t n_cap = 0;
+    DevBuf P[2], Q[2], M[2], R;          // n x 64 doubles / uint64 masks / 64 x n rho
+    DevBuf ulist[2], ucount, flag, tflag, tlist, tcount;
+    DevBuf col_src, col_tau, degsum[2], tt, ctrl;  // per-column state
+    DevBuf tau_slot, slot_edge_d, g_hat, s_hat, rho1;
+    DevBuf tiles, slots, partials;
+    cudaStream_t stream = nullptr;
+    uint64_t* h_ctrl = nullptr;  // pinned mirror of the control block
+    ~AescState() {
+        if (stream) cudaStreamDestroy(stream);
+        if (h_ctrl) cudaFreeHost(h_ctrl);
+    }
+};
+
 void release_aesc_state(saba_cu_graph* g) {
     delete g->aesc;
     g->aesc = nullptr;
 }
+
+namespace {
+
+// Control block (device): active mask, frozen-at-this-depth mask, dense flag.
+enum { kActive = 0, kFrozenNow = 1, kDense = 2, kCtrlWords = 4 };
+
+struct AescParams {
+    double eps, delta, log_term;  // log_term = log(4m/delta) (aesc.hpp:109)
+    double bip_init;
+    int64_t cap;
+    uint32_t n;
+    uint64_t m;
+    int uniform_tau;
+    uint32_t tau_uniform;
+};
+
+// walks_needed_raw (aesc.hpp:103-110) with the host's log term: the same
+// IEEE operations in the same order (device code is built with --fmad=false).
+__device__ __forceinline__ double walks_needed(int64_t tau_eff, double eps, double log_term,
+                                               uint32_t deg) {
+    if (tau_eff <= 0) return 0.0;
+    const double scale = 0.5 * eps * double(deg);
+    const double t = double(tau_eff);
+    return ceil((2.0 * t * t / (scale * scale)) * log_term);
+}
+
+// source_budget_sum (aesc.hpp:362-374): repeated addition over the slots.
+__device__ double budget_exact(const AescParams& p, const uint2* csr, const uint32_t* tau_slot,
+                               uint32_t src, uint32_t l) {
+    const uint2 r = csr[src];
+    double total = 0.0;
+    for (uint32_t s = r.x; s < r.x + r.y; ++s)
+        total += walks_needed(int64_t(tau_slot[s]) - int64_t(l), p.eps, p.log_term, r.y);
+    return total;
+}
+
+// (double)degsum >= budget, decided exactly. With a uniform tau the budget is
+// `deg` additions of one value x; |fl-sum - deg*x| <= deg^2 * x * 2^-53, so
+// the product decides the comparison unless degsum falls inside that band.
+__device__ bool budget_reached(const AescParams& p, const uint2* csr, const uint32_t* tau_slot,
+                               uint32_t src, uint32_t l, uint64_t degsum) {
+    const double ds = double(degsum);  // aesc.hpp:392
+    if (p.uniform_tau) {
+        const uint32_t deg = csr[src].y;
+        const double x = walks_needed(int64_t(p.tau_uniform) - int64_t(l), p.eps, p.log_term, deg);
+        const double est = double(deg) * x;
+        const double band = double(deg) * double(deg) * x * 0x1.0p-50;
+        if (ds >= est + band) return true;
+        if (ds < est - band) return false;
+    }
+    return ds >= budget_exact(p, csr, tau_slot, src, l);
+}
+
+__global__ void aesc_init(const uint32_t* __restrict__ col_src, int ncols,
+                          const uint2* __restrict__ csr, AescParams p, double* __restrict__ P,
+                          double* __restrict__ Q, unsigned long long* __restrict__ M,
+                          uint32_t* __restrict__ ulist, uint32_t* __restrict__ ucount,
+                          uint32_t* __restrict__ tflag, uint32_t* __restrict__ tlist,
+                          uint32_t* __restrict__ tcount, unsigned long long* __restrict__ degsum,
+                          uint32_t* __restrict__ tt, unsigned long long* __restrict__ ctrl,
+                          double* __restrict__ g_hat) {
+    const int c = threadIdx.x;
+    if (c < ncols) {
+        const uint32_t v = col_src[c];
+        const uint2 r = csr[v];
+        P[size_t(v) * kCols + c] = 1.0;
+        Q[size_t(v) * kCols + c] = 1.0 / double(r.y);  // share = val / deg (aesc.hpp:314)
+        M[v] = 1ull << c;  // the sources of a batch are distinct vertices
+        ulist[c] = v;
+        tflag[v] = 1;
+        tlist[c] = v;
+        degsum[c] = r.y;  // aesc.hpp:300
+        tt[c] = 0xffffffffu;
+        const double init = 1.0 / double(r.y) + p.bip_init;  // inv_deg + bip (aesc.hpp:577, 656)
+        for (uint32_t s = r.x; s < r.x + r.y; ++s) g_hat[s] = init;
+    }
+    if (c == 0) {
+        *ucount = ncols;
+        *tcount = ncols;
+        ctrl[kActive] = ncols == 64 ? ~0ull : ((1ull << ncols) - 1);
+        ctrl[kFrozenNow] = 0;
+        ctrl[kDense] = 0;
+    }
+}
+
+// One thread per column.
+__global__ void aesc_check(uint32_t l, const uint32_t* __restrict__ col_src,
+                           const uint32_t* __restrict__ col_tau, const uint2* __restrict__ csr,
+                           const uint32_t* __restrict__ tau_slot, AescParams p,
+                           const unsigned long long* __restrict__ degsum_cur,
+                           unsigned long long* __restrict__ degsum_next, uint32_t* __restrict__ tt,
+                           unsigned long long* __restrict__ ctrl) {
+    __shared__ unsigned long long frozen;
+    const int c = threadIdx.x;
+    if (c == 0) frozen = 0;
+    __syncthreads();
+    const unsigned long long active = ctrl[kActive];
+    degsum_next[c] = 0;
+    if ((active >> c) & 1ull) {
+        const uint32_t src = col_src[c];
+        bool stop = l >= col_tau[c] || (p.cap >= 0 && int64_t(l) >= p.cap);
+        if (!stop) stop = budget_reached(p, csr, tau_slot, src, l, degsum_cur[c]);
+        if (stop) {
+            tt[c] = l;
+            atomicOr(&frozen, 1ull << c);
+        }
+    }
+    __syncthreads();
+    if (c == 0) {
+        ctrl[kFrozenNow] = frozen;
+        ctrl[kActive] = active & ~frozen;
+    }
+}
+
+// rho for the columns frozen at this depth; rows outside the support hold
+// exact zeros in P and therefore in R.
+__global__ void aesc_rho(const double* __restrict__ P, const uint2* __restrict__ csr,
+                         const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
+                         const unsigned long long* __restrict__ ctrl, uint32_t n,
+                         double* __restrict__ R) {
+    const unsigned long long fz = ctrl[kFrozenNow];
+    if (!fz) return;
+    const bool dense = ctrl[kDense] != 0;
+    const uint32_t rows = dense ? n : *ucount;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+        const uint32_t v = dense ? i : ulist[i];
+        const double inv = 1.0 / double(csr[v].y);
+        unsigned long long f = fz;
+        while (f) {
+            const int c = __ffsll(f) - 1;
+            f &= f - 1;
+            R[size_t(c) * n + v] = P[size_t(v) * kCols + c] * inv;  // p * inv_deg (aesc.hpp:599)
+        }
+    }
+}
+
+// Sparse frontier growth: rows of depth l+1 = N(rows of depth l that still
+// carry an active column). Warp per row; the order of the new list is
+// irrelevant (every row is computed independently).
+__global__ void aesc_expand(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                            const unsigned long long* __restrict__ M,
+                            const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
+                            uint32_t* __restrict__ ulist_next, uint32_t* __restrict__ ucount_next,
+                            uint32_t* __restrict__ flag, uint32_t* __restrict__ tflag,
+                            uint32_t* __restrict__ tlist, uint32_t* __restrict__ tcount,
+                            const unsigned long long* __restrict__ ctrl) {
+    const unsigned long long active = ctrl[kActive];
+    if (!active || ctrl[kDense]) return;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t rows = *ucount;
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < rows;
+         i += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t v = ulist[i];
+        if (!(M[v] & active)) continue;
+        const uint2 r = csr[v];
+        for (uint32_t s = r.x + lane; s < r.x + r.y; s += 32) {
+            const uint32_t x = adj[s];
+            if (flag[x] || atomicExch(flag + x, 1u)) continue;
+            ulist_next[atomicAdd(ucount_next, 1u)] = x;
+            if (!tflag[x]) {  // x is claimed by exactly one thread per depth
+                tflag[x] = 1;
+                tlist[atomicAdd(tcount, 1u)] = x;
+            }
+        }
+    }
+}
+
+// Pull SpMM over the candidate rows (sparse) or all rows (dense). Warp per
+// row, lane = columns {2 lane, 2 lane + 1}; neighbours in ascending order.
+__global__ void __launch_bounds__(256)
+    aesc_pull(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+              const double* __restrict__ Qc, const unsigned long long* __restrict__ Mc,
+              double* __restrict__ Pn, double* __restrict__ Qn, unsigned long long* __restrict__ Mn,
+              const uint32_t* __restrict__ ulist_next, const uint32_t* __restrict__ ucount_next,
+              uint32_t* __restrict__ flag, unsigned long long* __restrict__ degsum_next,
+              unsigned long long* __restrict__ ctrl, uint32_t n) {
+    const unsigned long long active = ctrl[kActive];
+    if (!active) return;
+    const bool dense = ctrl[kDense] != 0;
+    const uint32_t rows = dense ? n : *ucount_next;
+    const uint32_t lane = threadIdx.x & 31;
+    const unsigned long long lo_mask = 1ull << (2 * lane), hi_mask = 1ull << (2 * lane + 1);
+    const bool act0 = (active & lo_mask) != 0, act1 = (active & hi_mask) != 0;
+    unsigned long long ds0 = 0, ds1 = 0;
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < rows;
+         i += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t x = dense ? i : ulist_next[i];
+        const uint2 r = csr[x];
+        double a0 = 0.0, a1 = 0.0;
+        unsigned long long mask = 0;
+        for (uint32_t s0 = r.x; s0 < r.x + r.y; s0 += 32) {
+            const uint32_t cnt = min(32u, r.x + r.y - s0);
+            const uint32_t mine = lane < cnt ? adj[s0 + lane] : 0u;
+            for (uint32_t k = 0; k < cnt; ++k) {
+                const uint32_t v = __shfl_sync(0xffffffffu, mine, k);
+                mask |= Mc[v];
+                const double2 q = reinterpret_cast<const double2*>(Qc + size_t(v) * kCols)[lane];
+                a0 += q.x;
+                a1 += q.y;
+            }
+        }
+        mask &= active;
+        if (!act0) a0 = 0.0;
+        if (!act1) a1 = 0.0;
+        const double dx = double(r.y);
+        reinterpret_cast<double2*>(Pn + size_t(x) * kCols)[lane] = make_double2(a0, a1);
+        reinterpret_cast<double2*>(Qn + size_t(x) * kCols)[lane] = make_double2(a0 / dx, a1 / dx);
+        if (lane == 0) {
+            Mn[x] = mask;
+            if (!dense) flag[x] = 0;
+        }
+        if (mask & lo_mask) ds0 += r.y;
+        if (mask & hi_mask) ds1 += r.y;
+    }
+    if (ds0) atomicAdd(degsum_next + 2 * lane, ds0);  // integer: order-free
+    if (ds1) atomicAdd(degsum_next + 2 * lane + 1, ds1);
+    // switch to dense rows once the frontier covers a quarter of the graph
+    if (!dense && blockIdx.x == 0 && threadIdx.x == 0 && rows > n / 4) ctrl[kDense] = 1;
+}
+
+// Hook (aesc.hpp:581-588) at depth l+1 for the columns that just stepped.
+__global__ void aesc_hook(uint32_t depth, const uint32_t* __restrict__ col_src,
+                          const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                          const uint32_t* __restrict__ tau_slot, const double* __restrict__ Pn,
+                          const unsigned long long* __restrict__ ctrl, double* __restrict__ g_hat) {
+    const int c = blockIdx.x;
+    if (!((ctrl[kActive] >> c) & 1ull)) return;
+    const uint32_t src = col_src[c];
+    const uint2 r = csr[src];
+    const double pi = Pn[size_t(src) * kCols + c] * (1.0 / double(r.y));
+    for (uint32_t s = r.x + threadIdx.x; s < r.x + r.y; s += blockDim.x) {
+        if (depth > tau_slot[s]) continue;
+        const uint32_t j = adj[s];
+        g_hat[s] += pi - Pn[size_t(j) * kCols + c] * (1.0 / double(csr[j].y));
+    }
+}
+
+// Restore the all-zero invariant on every row a sparse batch touched.
+__global__ void aesc_clear(const uint32_t* __restrict__ tlist, const uint32_t* __restrict__ tcount,
+                           double* P0, double* P1, double* Q0, double* Q1,
+                           unsigned long long* M0, unsigned long long* M1, double* R, uint32_t n,
+                           uint32_t* tflag, int ncols) {
+    const uint32_t rows = *tcount;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < rows;
+         i += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t x = tlist[i];
+        const double2 z = make_double2(0.0, 0.0);
+        reinterpret_cast<double2*>(P0 + size_t(x) * kCols)[lane] = z;
+        reinterpret_cast<double2*>(P1 + size_t(x) * kCols)[lane] = z;
+        reinterpret_cast<double2*>(Q0 + size_t(x) * kCols)[lane] = z;
+        reinterpret_cast<double2*>(Q1 + size_t(x) * kCols)[lane] = z;
+        for (int c = lane; c < ncols; c += 32) R[size_t(c) * n + x] = 0.0;
+        if (lane == 0) {
+            M0[x] = 0;
+            M1[x] = 0;
+            tflag[x] = 0;
+        }
+    }
+}
+
+struct WalkTile {
+    uint64_t k0;         // first pair index of the tile
+    uint64_t edge_seed;  // substream(src_seed, slot) (aesc.hpp:622)
+    double inv_n;        // 1 / n_req (aesc.hpp:512)
+    uint32_t vi, vj;     // side 0 / side 1 start vertices
+    uint32_t count;      // pairs in this tile (<= kTile)
+    uint32_t len;        // tau_eff + 1
+    uint32_t col;        // rho column
+    uint32_t pad;
+};
+
+struct SlotWork {
+    uint32_t t0, t1;  // tile range
+    uint32_t slot;    // directed slot receiving the estimate
+    uint32_t pad;
+};
+
+// K4: one tile per block iteration (persistent grid-stride).
+template <bool PACKED>
+__global__ void __launch_bounds__(kTileThreads)
+    aesc_walk(const WalkTile* __restrict__ tiles, uint32_t ntiles, const uint2* __restrict__ csr,
+              const uint32_t* __restrict__ adj, const uint64_t* __restrict__ adjp,
+              const double* __restrict__ R, uint32_t n, uint64_t mult,
+              double* __restrict__ partials) {
+    using Sort = cub::BlockRadixSort<uint32_t, kTileThreads, kTileIPT, uint32_t>;
+    using Reduce = cub::BlockReduce<double, kTileThreads, cub::BLOCK_REDUCE_WARP_REDUCTIONS>;
+    __shared__ union {
+        typename Sort::TempStorage sort;
+        double score1[kTile];
+        typename Reduce::TempStorage reduce;
+    } sm;
+    __shared__ double score0[kTile];
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        const WalkTile t = tiles[ti];
+        const double* rho = R + size_t(t.col) * n;
+        const uint32_t groups = (t.count + kTileThreads - 1) / kTileThreads;  // block-uniform
+        for (uint32_t side = 0; side < 2; ++side) {
+            uint32_t key[kTileIPT], item[kTileIPT];
+#pragma unroll
+            for (int i = 0; i < kTileIPT; ++i) {
+                const uint32_t it = tid * kTileIPT + i;
+                item[i] = it < t.count ? it : 0xffffffffu;
+                // walk seed counter_hash(edge_seed, 2k+side) >> 32 (aesc.hpp:485)
+                key[i] = it < t.count ? walk_seed(t.edge_seed, 2 * (t.k0 + it) + side) : 0xffffffffu;
+            }
+            // SABA: sort the tile's seeds so a warp holds 32 adjacent seeds
+            // (the top 16 bits decide the bouquet clustering; the order never
+            // affects a score)
+            __syncthreads();
+            Sort(sm.sort).SortBlockedToStriped(key, item, 16, 32);
+            __syncthreads();
+            const uint32_t start = side ? t.vj : t.vi;
+            uint32_t cur[kTileIPT];
+            double sc[kTileIPT];
+#pragma unroll
+            for (int i = 0; i < kTileIPT; ++i) {
+                cur[i] = start;
+                sc[i] = 0.0;
+            }
+            for (uint32_t l = 1; l < t.len; ++l) {
+                uint2 rec[kTileIPT];
+#pragma unroll
+                for (int i = 0; i < kTileIPT; ++i)
+                    if (i < groups) rec[i] = ldg_csr(csr + cur[i]);
+#pragma unroll
+                for (int i = 0; i < kTileIPT; ++i)
+                    if (i < groups) {
+                        const uint32_t raw = key[i] ^ hash_state(mult, cur[i], l);
+                        cur[i] = adj_at<PACKED>(adj, adjp, rec[i].x + scaled_index(raw, rec[i].y));
+                    }
+#pragma unroll
+                for (int i = 0; i < kTileIPT; ++i)
+                    if (i < groups) sc[i] += __ldg(rho + cur[i]);  // step order (aesc.hpp:492)
+            }
+            double* dst = side ? sm.score1 : score0;
+#pragma unroll
+            for (int i = 0; i < kTileIPT; ++i)
+                if (item[i] != 0xffffffffu) dst[item[i]] = sc[i];
+            __syncthreads();
+        }
+        double x = 0.0;
+#pragma unroll
+        for (int i = 0; i < kTileIPT; ++i) {
+            const uint32_t it = tid * kTileIPT + i;
+            if (it < t.count) x += (score0[it] - sm.score1[it]) * t.inv_n;  // aesc.hpp:522
+        }
+        __syncthreads();  // score1 aliases the reduce storage
+        const double tot = Reduce(sm.reduce).Sum(x);
+        if (tid == 0) partials[ti] = tot;
+        __syncthreads();
+    }
+}
+
+__global__ void aesc_slot_reduce(const SlotWork* __restrict__ sw, uint32_t nslots,
+                                 const double* __restrict__ partials, double* __restrict__ g_hat) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nslots; i += gridDim.x * blockDim.x) {
+        const SlotWork w = sw[i];
+        double acc = 0.0;
+        for (uint32_t t = w.t0; t < w.t1; ++t) acc += partials[t];
+        g_hat[w.slot] += acc;
+    }
+}
+
+__global__ void aesc_symmetrise(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                                const uint32_t* __restrict__ slot_edge, uint32_t n,
+                                const double* __restrict__ g_hat, double* __restrict__ s_hat) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        const uint2 r = csr[u];
+        for (uint32_t s = r.x; s < r.x + r.y; ++s) {
+            const uint32_t v = adj[s];
+            if (v <= u) continue;
+            const uint2 rv = csr[v];
+            uint32_t lo = rv.x, hi = rv.x + rv.y;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (adj[mid] < u) lo = mid + 1; else hi = mid;
+            }
+            s_hat[slot_edge[s]] = g_hat[s] + g_hat[lo];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host
+
+template <class T>
+T* buf(DevBuf& b, size_t count) {
+    return static_cast<T*>(b.ensure(sizeof(T) * (count ? count : 1)));
+}
+
+struct Engine {
+    saba_cu_graph* g;
+    AescState* st;
+    cudaStream_t s;
+    AescParams p{};
+    std::vector<uint32_t> tau_slot;  // host copy, per directed slot
+    uint32_t launches = 0;
+    uint64_t pairs = 0, steps = 0;
+
+    explicit Engine(saba_cu_graph* g_) : g(g_) {
+        if (!g->aesc) g->aesc = new AescState;
+        st = g->aesc;
+        if (!st->stream) {
+            SABA_CUDA_CHECK(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+            SABA_CUDA_CHECK(cudaHostAlloc(&st->h_ctrl, sizeof(uint64_t) * kCtrlWords, cudaHostAllocDefault));
+        }
+        s = st->stream;
+        const uint32_t n = g->n;
+        if (st->n_cap < n) {
+            const size_t rows = size_t(n) * kCols;
+            for (int b = 0; b < 2; ++b) {
+                SABA_CUDA_CHECK(cudaMemsetAsync(buf<double>(st->P[b], rows), 0, sizeof(double) * rows, s));
+                SABA_CUDA_CHECK(cudaMemsetAsync(buf<double>(st->Q[b], rows), 0, sizeof(double) * rows, s));
+                SABA_CUDA_CHECK(cudaMemsetAsync(buf<uint64_t>(st->M[b], n), 0, sizeof(uint64_t) * n, s));
+                buf<uint32_t>(st->ulist[b], n);
+            }
+            SABA_CUDA_CHECK(cudaMemsetAsync(buf<double>(st->R, rows), 0, sizeof(double) * rows, s));
+            SABA_CUDA_CHECK(cudaMemsetAsync(buf<uint32_t>(st->flag, n), 0, sizeof(uint32_t) * n, s));
+            SABA_CUDA_CHECK(cudaMemsetAsync(buf<uint32_t>(st->tflag, n), 0, sizeof(uint32_t) * n, s));
+            buf<uint32_t>(st->tlist, n);
+            st->n_cap = n;
+        }
+        buf<uint32_t>(st->ucount, 2);
+        buf<uint32_t>(st->tcount, 1);
+        buf<uint32_t>(st->col_src, kCols);
+        buf<uint32_t>(st->col_tau, kCols);
+        buf<uint64_t>(st->degsum[0], kCols);
+        buf<uint64_t>(st->degsum[1], kCols);
+        buf<uint32_t>(st->tt, kCols);
+        buf<uint64_t>(st->ctrl, kCtrlWords);
+    }
+
+    void upload_tau(std::vector<uint32_t> ts) {
+        tau_slot = std::move(ts);
+        SABA_CUDA_CHECK(cudaMemcpyAsync(buf<uint32_t>(st->tau_slot, tau_slot.size()), tau_slot.data(),
+                                        sizeof(uint32_t) * tau_slot.size(), cudaMemcpyHostToDevice, s));
+    }
+
+    uint32_t deg(uint32_t v) const { return g->h_off[v + 1] - g->h_off[v]; }
+
+    uint64_t read_ctrl(int word) {
+        SABA_CUDA_CHECK(cudaMemcpyAsync(st->h_ctrl + word, st->ctrl.as<uint64_t>() + word,
+                                        sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        SABA_CUDA_CHECK(cudaStreamSynchronize(s));
+        return st->h_ctrl[word];
+    }
+
+    // Propagation of one batch (advance_to_switch for every column); returns
+    // tau~ per column. *parity = index of the P buffer holding p_tau~.
+    std::vector<uint32_t> propagate(const std::vector<uint32_t>& cols, double* g_hat_dev,
+                                    int* parity = nullptr) {
+        const int nc = int(cols.size());
+        const uint32_t n = g->n;
+        std::vector<uint32_t> ctau(nc);
+        uint32_t lmax = 0;
+        for (int c = 0; c < nc; ++c) {
+            uint32_t t = 0;
+            for (uint32_t sl = g->h_off[cols[c]]; sl < g->h_off[cols[c] + 1]; ++sl)
+                t = std::max(t, tau_slot[sl]);
+            ctau[c] = t;  // tau_src (aesc.hpp:386-388)
+            lmax = std::max(lmax, t);
+        }
+        if (p.cap >= 0) lmax = uint32_t(std::min<int64_t>(lmax, p.cap));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(st->col_src.p, cols.data(), sizeof(uint32_t) * nc, cudaMemcpyHostToDevice, s));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(st->col_tau.p, ctau.data(), sizeof(uint32_t) * nc, cudaMemcpyHostToDevice, s));
+        double* P[2] = {st->P[0].as<double>(), st->P[1].as<double>()};
+        double* Q[2] = {st->Q[0].as<double>(), st->Q[1].as<double>()};
+        unsigned long long* M[2] = {st->M[0].as<unsigned long long>(), st->M[1].as<unsigned long long>()};
+        uint32_t* UL[2] = {st->ulist[0].as<uint32_t>(), st->ulist[1].as<uint32_t>()};
+        uint32_t* UC = st->ucount.as<uint32_t>();
+        unsigned long long* DS[2] = {st->degsum[0].as<unsigned long long>(),
+                                     st->degsum[1].as<unsigned long long>()};
+        auto* ctrl = st->ctrl.as<unsigned long long>();
+        const uint2* csr = g->d_csr;
+        const uint32_t* adj = g->d_adj;
+        const uint32_t* tsl = st->tau_slot.as<uint32_t>();
+        uint32_t* flag = st->flag.as<uint32_t>();
+        uint32_t* tflag = st->tflag.as<uint32_t>();
+        uint32_t* tlist = st->tlist.as<uint32_t>();
+        uint32_t* tcount = st->tcount.as<uint32_t>();
+        uint32_t* ttd = st->tt.as<uint32_t>();
+        aesc_init<<<1, kCols, 0, s>>>(st->col_src.as<uint32_t>(), nc, csr, p, P[0], Q[0], M[0], UL[0],
+                                      UC, tflag, tlist, tcount, DS[0], ttd, ctrl, g_hat_dev);
+        ++launches;
+        const int grid = g->sm_count * 8;
+        int cur = 0;
+        for (uint32_t l = 0;; ++l) {
+            aesc_check<<<1, kCols, 0, s>>>(l, st->col_src.as<uint32_t>(), st->col_tau.as<uint32_t>(),
+                                           csr, tsl, p, DS[cur], DS[cur ^ 1], ttd, ctrl);
+            aesc_rho<<<grid, 256, 0, s>>>(P[cur], csr, UL[cur], UC + cur, ctrl, n, st->R.as<double>());
+            launches += 2;
+            if (l >= lmax) break;
+            // poll the active mask: every depth early on, then every 4 depths
+            if ((l < 4 || (l & 3) == 0) && read_ctrl(kActive) == 0) break;
+            SABA_CUDA_CHECK(cudaMemsetAsync(UC + (cur ^ 1), 0, sizeof(uint32_t), s));
+            aesc_expand<<<grid, 256, 0, s>>>(csr, adj, M[cur], UL[cur], UC + cur, UL[cur ^ 1],
+                                             UC + (cur ^ 1), flag, tflag, tlist, tcount, ctrl);
+            aesc_pull<<<grid, 256, 0, s>>>(csr, adj, Q[cur], M[cur], P[cur ^ 1], Q[cur ^ 1], M[cur ^ 1],
+                                           UL[cur ^ 1], UC + (cur ^ 1), flag, DS[cur ^ 1], ctrl, n);
+            aesc_hook<<<nc, 128, 0, s>>>(l + 1, st->col_src.as<uint32_t>(), csr, adj, tsl, P[cur ^ 1],
+                                         ctrl, g_hat_dev);
+            launches += 3;
+            cur ^= 1;
+        }
+        SABA_CUDA_CHECK(cudaGetLastError());
+        if (parity) *parity = cur;
+        std::vector<uint32_t> tt(nc);
+        SABA_CUDA_CHECK(cudaMemcpyAsync(tt.data(), ttd, sizeof(uint32_t) * nc, cudaMemcpyDeviceToHost, s));
+        SABA_CUDA_CHECK(cudaStreamSynchronize(s));
+        return tt;
+    }
+
+    void clear_batch(int nc) {
+        const uint32_t n = g->n;
+        if (read_ctrl(kDense)) {  // dense batches touched every row
+            const size_t rows = size_t(n) * kCols;
+            for (int b = 0; b < 2; ++b) {
+                SABA_CUDA_CHECK(cudaMemsetAsync(st->P[b].p, 0, sizeof(double) * rows, s));
+                SABA_CUDA_CHECK(cudaMemsetAsync(st->Q[b].p, 0, sizeof(double) * rows, s));
+                SABA_CUDA_CHECK(cudaMemsetAsync(st->M[b].p, 0, sizeof(uint64_t) * n, s));
+            }
+            SABA_CUDA_CHECK(cudaMemsetAsync(st->R.p, 0, sizeof(double) * size_t(n) * nc, s));
+            SABA_CUDA_CHECK(cudaMemsetAsync(st->tflag.p, 0, sizeof(uint32_t) * n, s));
+            return;
+        }
+        aesc_clear<<<g->sm_count * 8, 256, 0, s>>>(
+            st->tlist.as<uint32_t>(), st->tcount.as<uint32_t>(), st->P[0].as<double>(),
+            st->P[1].as<double>(), st->Q[0].as<double>(), st->Q[1].as<double>(),
+            st->M[0].as<unsigned long long>(), st->M[1].as<unsigned long long>(), st->R.as<double>(),
+            n, st->tflag.as<uint32_t>(), nc);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        ++launches;
+    }
+};
+
+void validate_cfg(const saba_cu_aesc_config& c) {
+    // aesc.hpp:637-641 (same order)
+    check_arg(c.epsilon > 0.0 && c.epsilon < 1.0, "aesc: epsilon must be in (0,1)");
+    check_arg(c.delta > 0.0 && c.delta < 1.0, "aesc: delta must be in (0,1)");
+    check_arg(c.power_iterations >= 1, "aesc: omega must be >= 1");
+    check_arg(c.lanes >= 1 && c.lanes <= 64 && (c.lanes & (c.lanes - 1)) == 0,
+              "aesc: lanes must be a power of two in [1, 64]");
+    check_arg(c.mode == SABA_MODE_HASH || c.mode == SABA_MODE_SABA,
+              "aesc: mode not supported on GPU (naive/vector-mod are CPU LCG baselines)");
+}
+
+struct TileBuilder {
+    std::vector<WalkTile> tiles;
+    std::vector<SlotWork> slots;
+    void add(uint32_t slot, uint32_t vi, uint32_t vj, uint32_t len, uint64_t n_req, uint64_t edge_seed,
+             uint32_t col) {
+        SlotWork w{uint32_t(tiles.size()), 0, slot, 0};
+        const double inv_n = 1.0 / double(n_req);
+        for (uint64_t k0 = 0; k0 < n_req; k0 += kTile) {
+            WalkTile t{};
+            t.k0 = k0;
+            t.edge_seed = edge_seed;
+            t.inv_n = inv_n;
+            t.vi = vi;
+            t.vj = vj;
+            t.count = uint32_t(std::min<uint64_t>(kTile, n_req - k0));
+            t.len = len;
+            t.col = col;
+            tiles.push_back(t);
+        }
+        w.t1 = uint32_t(tiles.size());
+        slots.push_back(w);
+    }
+};
+
+void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, const TileBuilder& tb,
+               const double* R, uint64_t mult, double* g_hat_dev, uint32_t* launches) {
+    if (tb.tiles.empty()) return;
+    WalkTile* dt = static_cast<WalkTile*>(st->tiles.ensure(sizeof(WalkTile) * tb.tiles.size()));
+    SlotWork* ds = static_cast<SlotWork*>(st->slots.ensure(sizeof(SlotWork) * tb.slots.size()));
+    double* part = static_cast<double*>(st->partials.ensure(sizeof(double) * tb.tiles.size()));
+    SABA_CUDA_CHECK(cudaMemcpyAsync(dt, tb.tiles.data(), sizeof(WalkTile) * tb.tiles.size(),
+                                    cudaMemcpyHostToDevice, s));
+    SABA_CUDA_CHECK(cudaMemcpyAsync(ds, tb.slots.data(), sizeof(SlotWork) * tb.slots.size(),
+                                    cudaMemcpyHostToDevice, s));
+    const bool packed = g->d_adj_packed != nullptr;
+    int occ = 0;
+    if (packed)
+        SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk<true>, kTileThreads, 0));
+    else
+        SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk<false>, kTileThreads, 0));
+    const uint32_t nt = uint32_t(tb.tiles.size());
+    const int grid = int(std::min<uint64_t>(nt, uint64_t(g->sm_count) * std::max(occ, 1)));
+    if (packed)
+        aesc_walk<true><<<grid, kTileThreads, 0, s>>>(dt, nt, g->d_csr, g->d_adj, g->d_adj_packed, R,
+                                                      g->n, mult, part);
+    else
+        aesc_walk<false><<<grid, kTileThreads, 0, s>>>(dt, nt, g->d_csr, g->d_adj, g->d_adj_packed, R,
+                                                       g->n, mult, part);
+    SABA_CUDA_CHECK(cudaGetLastError());
+    const uint32_t nsw = uint32_t(tb.slots.size());
+    aesc_slot_reduce<<<(nsw + 127) / 128, 128, 0, s>>>(ds, nsw, part, g_hat_dev);
+    SABA_CUDA_CHECK(cudaGetLastError());
+    *launches += 2;
+    // the host tile vectors are reused by the caller: finish the uploads first
+    SABA_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+AescParams make_params(const saba_cu_graph* g, double eps, double delta, int64_t cap) {
+    AescParams p{};
+    p.eps = eps;
+    p.delta = delta;
+    p.log_term = std::log(4.0 * double(g->m) / delta);  // aesc.hpp:109
+    p.cap = cap;
+    p.n = g->n;
+    p.m = g->m;
+    return p;
+}
+
+}  // namespace
 }  // namespace saba_cu
 
 using namespace saba_cu;
@@ -19,7 +704,7 @@ int saba_cu_truncated_lengths(saba_cu_graph* g, double epsilon, uint32_t power_i
                               double* lambda_hat, int* clamped) {
     return guard([&] {
         check_arg(g && tau_out && lambda_hat && clamped, "null argument");
-        const HostCsr h{g->n, g->m, g->h_off.data(), g->h_adj.data()};
+        const HostCsr h{g->n, g->m, g->h_off.data(), host_adj(g).data()};
         const Plan p = host_truncated_lengths(h, slot_edges(g), epsilon, power_iterations,
                                               max_truncation, per_edge != 0);
         std::copy(p.tau.begin(), p.tau.end(), tau_out);
@@ -28,19 +713,187 @@ int saba_cu_truncated_lengths(saba_cu_graph* g, double epsilon, uint32_t power_i
     });
 }
 
-int saba_cu_aesc(saba_cu_graph*, const saba_cu_aesc_config*, const uint32_t*, uint64_t, uint32_t,
-                 uint32_t, double*, double*, uint32_t*, uint32_t*, saba_cu_aesc_report*) {
-    return guard([&] { throw ArgError("aesc: not implemented yet"); });
+int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_t* sources,
+                 uint64_t source_count, uint32_t shard_index, uint32_t shard_count,
+                 double* g_hat_out, double* s_hat_out, uint32_t* tau_out, uint32_t* tau_tilde_out,
+                 saba_cu_aesc_report* rep) {
+    return guard([&] {
+        check_arg(g && cfg && g_hat_out && tau_out && tau_tilde_out, "null argument");
+        validate_cfg(*cfg);
+        check_arg(shard_count >= 1 && shard_index < shard_count, "bad shard index/count");
+        DeviceScope scope(g->device);
+        const auto t_plan0 = std::chrono::steady_clock::now();
+        const auto& hadj = host_adj(g);
+        const HostCsr h{g->n, g->m, g->h_off.data(), hadj.data()};
+        check_data(host_is_connected(h), "aesc: spanning centrality requires a connected graph");
+        const auto& se = slot_edges(g);
+        // aesc.hpp:649: the plan is built for epsilon / 2
+        const Plan plan = host_truncated_lengths(h, se, cfg->epsilon / 2.0, cfg->power_iterations,
+                                                 cfg->max_truncation, cfg->per_edge_tau != 0);
+        const auto t_plan1 = std::chrono::steady_clock::now();
+        const uint32_t n = g->n;
+        const uint64_t m = g->m;
+        for (uint64_t i = 0; i < source_count; ++i) check_arg(sources[i] < n, "source out of range");
+
+        Engine E(g);
+        E.p = make_params(g, cfg->epsilon, cfg->delta, cfg->switch_depth_cap);
+        E.p.bip_init = plan.bipartite ? 1.0 / (2.0 * double(m)) : 0.0;  // aesc.hpp:657
+        E.p.uniform_tau = plan.uniform ? 1 : 0;
+        E.p.tau_uniform = plan.tau.empty() ? 0 : plan.tau[0];
+        std::vector<uint32_t> ts(2 * m);
+        for (uint64_t s = 0; s < 2 * m; ++s) ts[s] = plan.tau[se[s]];
+        E.upload_tau(ts);
+        double* d_g = static_cast<double*>(E.st->g_hat.ensure(sizeof(double) * 2 * m));
+        SABA_CUDA_CHECK(cudaMemsetAsync(d_g, 0, sizeof(double) * 2 * m, E.s));
+
+        // this shard's sources, batched by descending degree (tau~ correlates
+        // with degree; batching never changes a column's arithmetic)
+        std::vector<uint32_t> list;
+        const uint64_t total = sources ? source_count : n;
+        for (uint64_t i = shard_index; i < total; i += shard_count)
+            list.push_back(sources ? sources[i] : uint32_t(i));
+        std::stable_sort(list.begin(), list.end(),
+                         [&](uint32_t a, uint32_t b) { return E.deg(a) > E.deg(b); });
+        std::vector<uint32_t> tt_all(n, 0);
+        cudaEvent_t e0, e1, e2;
+        SABA_CUDA_CHECK(cudaEventCreate(&e0));
+        SABA_CUDA_CHECK(cudaEventCreate(&e1));
+        SABA_CUDA_CHECK(cudaEventCreate(&e2));
+        float prop_ms = 0.f, walk_ms = 0.f;
+        const auto t0 = std::chrono::steady_clock::now();
+        TileBuilder tb;
+        for (size_t b0 = 0; b0 < list.size(); b0 += kCols) {
+            const std::vector<uint32_t> cols(list.begin() + b0,
+                                             list.begin() + std::min(list.size(), b0 + kCols));
+            SABA_CUDA_CHECK(cudaEventRecord(e0, E.s));
+            const std::vector<uint32_t> tt = E.propagate(cols, d_g);
+            SABA_CUDA_CHECK(cudaEventRecord(e1, E.s));
+            tb.tiles.clear();
+            tb.slots.clear();
+            for (size_t c = 0; c < cols.size(); ++c) {
+                const uint32_t src = cols[c];
+                tt_all[src] = tt[c];
+                const uint32_t lo = g->h_off[src], hi = g->h_off[src + 1], deg_i = hi - lo;
+                bool any = false;  // aesc.hpp:592-594
+                for (uint32_t sl = lo; sl < hi && !any; ++sl) any = ts[sl] > tt[c];
+                if (!any) continue;
+                const uint64_t src_seed = substream(substream(cfg->master_seed, kAescTag), src);
+                for (uint32_t sl = lo; sl < hi; ++sl) {
+                    const int64_t tau_eff = int64_t(ts[sl]) - int64_t(tt[c]);
+                    if (tau_eff <= 0) continue;
+                    const uint64_t n_req = walk_budget(uint32_t(tau_eff), cfg->epsilon, cfg->delta, deg_i, m);
+                    check_arg(cfg->switch_depth_cap < 0 || n_req * uint64_t(tau_eff) <= (uint64_t(1) << 26),
+                              "aesc: walk budget infeasible (switch_depth_cap too aggressive for epsilon)");
+                    tb.add(sl, src, hadj[sl], uint32_t(tau_eff + 1), n_req, substream(src_seed, sl),
+                           uint32_t(c));
+                    E.pairs += n_req;
+                    E.steps += 2 * n_req * uint64_t(tau_eff);
+                }
+            }
+            run_tiles(g, E.st, E.s, tb, E.st->R.as<double>(), cfg->hash_multiplier, d_g, &E.launches);
+            SABA_CUDA_CHECK(cudaEventRecord(e2, E.s));
+            E.clear_batch(int(cols.size()));
+            SABA_CUDA_CHECK(cudaEventSynchronize(e2));
+            float a = 0.f, b = 0.f;
+            SABA_CUDA_CHECK(cudaEventElapsedTime(&a, e0, e1));
+            SABA_CUDA_CHECK(cudaEventElapsedTime(&b, e1, e2));
+            prop_ms += a;
+            walk_ms += b;
+        }
+        const bool full = sources == nullptr && shard_count == 1;
+        if (full && s_hat_out) {
+            double* d_s = static_cast<double*>(E.st->s_hat.ensure(sizeof(double) * m));
+            uint32_t* d_se = static_cast<uint32_t*>(E.st->slot_edge_d.ensure(sizeof(uint32_t) * 2 * m));
+            SABA_CUDA_CHECK(cudaMemcpyAsync(d_se, se.data(), sizeof(uint32_t) * 2 * m, cudaMemcpyHostToDevice, E.s));
+            aesc_symmetrise<<<g->sm_count * 4, 256, 0, E.s>>>(g->d_csr, g->d_adj, d_se, n, d_g, d_s);
+            SABA_CUDA_CHECK(cudaGetLastError());
+            ++E.launches;
+            SABA_CUDA_CHECK(cudaMemcpyAsync(s_hat_out, d_s, sizeof(double) * m, cudaMemcpyDeviceToHost, E.s));
+        }
+        SABA_CUDA_CHECK(cudaMemcpyAsync(g_hat_out, d_g, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost, E.s));
+        SABA_CUDA_CHECK(cudaStreamSynchronize(E.s));
+        const auto t1 = std::chrono::steady_clock::now();
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+        std::copy(plan.tau.begin(), plan.tau.end(), tau_out);
+        std::copy(tt_all.begin(), tt_all.end(), tau_tilde_out);
+        if (rep) {
+            saba_cu_aesc_report r{};
+            r.seconds = std::chrono::duration<double>(t1 - t0).count();
+            r.plan_seconds = std::chrono::duration<double>(t_plan1 - t_plan0).count();
+            r.propagation_ms = prop_ms;
+            r.walk_ms = walk_ms;
+            r.total_walk_pairs = E.pairs;
+            r.total_walk_steps = E.steps;
+            r.sources = list.size();
+            r.lambda_hat = plan.lambda_hat;
+            r.bipartite = plan.bipartite;
+            r.clamped = plan.clamped;
+            r.max_tau = plan.max_tau;
+            r.launches = E.launches;
+            *rep = r;
+        }
+    });
 }
 
-int saba_cu_propagate(saba_cu_graph*, uint32_t, const uint32_t*, double, double, int64_t, double*,
-                      uint32_t*) {
-    return guard([&] { throw ArgError("propagate: not implemented yet"); });
+int saba_cu_propagate(saba_cu_graph* g, uint32_t source, const uint32_t* tau, double epsilon,
+                      double delta, int64_t cap, double* prob_out, uint32_t* depth_out) {
+    return guard([&] {
+        check_arg(g && tau && prob_out && depth_out, "null argument");
+        check_arg(source < g->n, "LandingPropagator: source out of range");
+        DeviceScope scope(g->device);
+        const HostCsr h{g->n, g->m, g->h_off.data(), host_adj(g).data()};
+        check_data(host_is_connected(h), "propagate_landing_probabilities: graph must be connected");
+        const auto& se = slot_edges(g);
+        Engine E(g);
+        E.p = make_params(g, epsilon, delta, cap);
+        E.p.uniform_tau = 0;  // caller-supplied tau: exact budget loop
+        std::vector<uint32_t> ts(2 * g->m);
+        for (uint64_t s = 0; s < 2 * g->m; ++s) ts[s] = tau[se[s]];
+        E.upload_tau(std::move(ts));
+        double* d_g = static_cast<double*>(E.st->g_hat.ensure(sizeof(double) * std::max<uint64_t>(2 * g->m, 1)));
+        const std::vector<uint32_t> tt = E.propagate({source}, d_g);
+        // column 0 of P at the switch depth: depth d always lives in P[d & 1]
+        std::vector<double> rows(size_t(g->n) * kCols);
+        SABA_CUDA_CHECK(cudaMemcpyAsync(rows.data(), E.st->P[tt[0] & 1].p, sizeof(double) * rows.size(),
+                                        cudaMemcpyDeviceToHost, E.s));
+        SABA_CUDA_CHECK(cudaStreamSynchronize(E.s));
+        for (uint32_t v = 0; v < g->n; ++v) prob_out[v] = rows[size_t(v) * kCols];
+        *depth_out = tt[0];
+        E.clear_batch(1);
+        SABA_CUDA_CHECK(cudaStreamSynchronize(E.s));
+    });
 }
 
-int saba_cu_estimate_edge(saba_cu_graph*, uint32_t, uint32_t, const double*, uint32_t, uint64_t, int,
-                          uint64_t, uint32_t, uint64_t, double*) {
-    return guard([&] { throw ArgError("estimate_edge: not implemented yet"); });
+int saba_cu_estimate_edge(saba_cu_graph* g, uint32_t v_i, uint32_t v_j, const double* prob,
+                          uint32_t tau_eff, uint64_t n_req, int mode, uint64_t edge_seed,
+                          uint32_t lanes, uint64_t mult, double* out) {
+    return guard([&] {
+        check_arg(tau_eff >= 1, "estimate_edge: tau_eff must be >= 1");  // aesc.hpp:537-538
+        check_arg(n_req >= 1, "estimate_edge: n_req must be >= 1");
+        check_arg(g && prob && out, "null argument");
+        check_arg(v_i < g->n && v_j < g->n, "vertex out of range");
+        check_arg(g->h_off[v_i + 1] > g->h_off[v_i] && g->h_off[v_j + 1] > g->h_off[v_j],
+                  "cannot walk from an isolated vertex");
+        check_arg(mode == SABA_MODE_HASH || mode == SABA_MODE_SABA, "mode not supported on GPU");
+        check_arg(lanes >= 1 && lanes <= 64, "lanes must be in [1, 64]");
+        DeviceScope scope(g->device);
+        Engine E(g);
+        // dense rho = p / degree (aesc.hpp:541-548 uses the division form here)
+        std::vector<double> rho(g->n);
+        for (uint32_t v = 0; v < g->n; ++v) rho[v] = prob[v] != 0.0 ? prob[v] / double(E.deg(v)) : 0.0;
+        double* d_rho = static_cast<double*>(E.st->rho1.ensure(sizeof(double) * g->n));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(d_rho, rho.data(), sizeof(double) * g->n, cudaMemcpyHostToDevice, E.s));
+        double* d_out = static_cast<double*>(E.st->s_hat.ensure(sizeof(double) * std::max<uint64_t>(g->m, 1)));
+        SABA_CUDA_CHECK(cudaMemsetAsync(d_out, 0, sizeof(double), E.s));
+        TileBuilder tb;
+        tb.add(0, v_i, v_j, tau_eff + 1, n_req, edge_seed, 0);
+        uint32_t launches = 0;
+        run_tiles(g, E.st, E.s, tb, d_rho, mult, d_out, &launches);
+        SABA_CUDA_CHECK(cudaMemcpyAsync(out, d_out, sizeof(double), cudaMemcpyDeviceToHost, E.s));
+        SABA_CUDA_CHECK(cudaStreamSynchronize(E.s));
+    });
 }
 
 }  // extern "C"

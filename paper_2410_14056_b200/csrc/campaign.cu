@@ -23,6 +23,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <string>
 
 #include "device_graph.cuh"
 #include "saba_hash.cuh"
@@ -74,11 +77,14 @@ __global__ void gen_keys_kernel(uint32_t n, const uint32_t* __restrict__ kv, uin
     }
 }
 
-template <int WPT>
+// CT = counter type: uint32 per-launch counters (half the L2 footprint of
+// uint64) whenever a launch cannot overflow them, flushed into the uint64
+// sink by add_counts_kernel. PACKED = 21-bit packed adjacency.
+template <int WPT, bool PACKED, class CT, bool AGG>
 __global__ void __launch_bounds__(kWalkThreads)
     walk_count_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
-                      const uint64_t* __restrict__ keys, uint64_t nwalks, uint32_t L, uint64_t mult,
-                      unsigned long long* __restrict__ counts) {
+                      const uint64_t* __restrict__ adjp, const uint64_t* __restrict__ keys,
+                      uint64_t nwalks, uint32_t L, uint64_t mult, CT* __restrict__ counts) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -101,14 +107,94 @@ __global__ void __launch_bounds__(kWalkThreads)
 #pragma unroll
             for (int r = 0; r < WPT; ++r) {
                 const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
-                nxt[r] = act[r] ? ldg_u32(adj + rec[r].x + scaled_index(raw, rec[r].y)) : 0u;
+                nxt[r] = act[r] ? adj_at<PACKED>(adj, adjp, rec[r].x + scaled_index(raw, rec[r].y)) : 0u;
             }
 #pragma unroll
             for (int r = 0; r < WPT; ++r) {
                 cur[r] = nxt[r];
-                warp_count_visit(counts, nxt[r], act[r], lane);
+                if constexpr (AGG)
+                    warp_count_visit(counts, nxt[r], act[r], lane);
+                else
+                    count_visit(counts, nxt[r], act[r]);
             }
         }
+    }
+}
+
+__global__ void add_counts_kernel(const uint32_t* __restrict__ c32, uint32_t n,
+                                  unsigned long long* __restrict__ counts) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint32_t c = c32[v];
+        if (c) counts[v] += c;
+    }
+}
+
+// Kernel variant (tuning knob; SABA_WALK_VARIANT="wpt=4,packed=1,c32=1,agg=1").
+struct WalkVariant {
+    int wpt = 4;
+    bool packed = true;
+    bool c32 = false;
+    bool agg = true;
+    int blocks_per_sm = 0;  // 0 = occupancy maximum
+};
+
+WalkVariant walk_variant() {
+    static WalkVariant v = [] {
+        WalkVariant w;
+        if (const char* e = getenv("SABA_WALK_VARIANT")) {
+            std::string s(e);
+            auto get = [&](const char* k, int def) {
+                const auto p = s.find(k);
+                return p == std::string::npos ? def : atoi(s.c_str() + p + strlen(k));
+            };
+            w.wpt = get("wpt=", w.wpt);
+            w.packed = get("packed=", w.packed) != 0;
+            w.c32 = get("c32=", w.c32) != 0;
+            w.agg = get("agg=", w.agg) != 0;
+            w.blocks_per_sm = get("bps=", 0);
+        }
+        return w;
+    }();
+    return v;
+}
+
+template <int WPT, bool P, class CT, bool A>
+void launch_walk_t(const saba_cu_graph* g, int bps, const uint64_t* keys, uint64_t nw, uint32_t L,
+                   uint64_t mult, void* counts, cudaStream_t st) {
+    auto k = walk_count_kernel<WPT, P, CT, A>;
+    int occ = 0;
+    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWalkThreads, 0));
+    if (bps <= 0 || bps > occ) bps = occ > 0 ? occ : 1;
+    k<<<g->sm_count * bps, kWalkThreads, 0, st>>>(g->d_csr, g->d_adj, g->d_adj_packed, keys, nw, L,
+                                                  mult, static_cast<CT*>(counts));
+    SABA_CUDA_CHECK(cudaGetLastError());
+}
+
+template <int WPT>
+void launch_walk_w(const saba_cu_graph* g, const WalkVariant& v, bool packed, bool c32,
+                   const uint64_t* keys, uint64_t nw, uint32_t L, uint64_t mult, void* counts,
+                   cudaStream_t st) {
+    using U64 = unsigned long long;
+#define SABA_LW(P, CT, A) launch_walk_t<WPT, P, CT, A>(g, v.blocks_per_sm, keys, nw, L, mult, counts, st)
+    if (packed) {
+        if (c32) { if (v.agg) SABA_LW(true, uint32_t, true); else SABA_LW(true, uint32_t, false); }
+        else { if (v.agg) SABA_LW(true, U64, true); else SABA_LW(true, U64, false); }
+    } else {
+        if (c32) { if (v.agg) SABA_LW(false, uint32_t, true); else SABA_LW(false, uint32_t, false); }
+        else { if (v.agg) SABA_LW(false, U64, true); else SABA_LW(false, U64, false); }
+    }
+#undef SABA_LW
+}
+
+void launch_walk(const saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, uint32_t L,
+                 uint64_t mult, void* counts, cudaStream_t st) {
+    const WalkVariant v = walk_variant();
+    const bool packed = v.packed && g->d_adj_packed != nullptr;
+    switch (v.wpt) {
+        case 1: launch_walk_w<1>(g, v, packed, c32, keys, nw, L, mult, counts, st); break;
+        case 2: launch_walk_w<2>(g, v, packed, c32, keys, nw, L, mult, counts, st); break;
+        case 8: launch_walk_w<8>(g, v, packed, c32, keys, nw, L, mult, counts, st); break;
+        default: launch_walk_w<4>(g, v, packed, c32, keys, nw, L, mult, counts, st); break;
     }
 }
 
@@ -131,18 +217,7 @@ __global__ void walk_paths_kernel(const uint2* __restrict__ csr, const uint32_t*
     }
 }
 
-constexpr int kWalksPerThread = 4;
 constexpr uint64_t kChunkWalks = uint64_t(1) << 27;  // keys per pass (1 GiB x2)
-
-int walk_grid(saba_cu_graph* g) {
-    static int blocks_per_sm = 0;
-    if (!blocks_per_sm) {
-        SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &blocks_per_sm, walk_count_kernel<kWalksPerThread>, kWalkThreads, 0));
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-    }
-    return g->sm_count * blocks_per_sm;
-}
 
 void validate_campaign(const saba_cu_graph* g, const saba_cu_campaign_config& c) {
     // walker.hpp:461-468, same order and messages
@@ -193,7 +268,9 @@ uint64_t enqueue_campaign(saba_cu_graph* g, const saba_cu_campaign_config& c,
                              ? static_cast<uint64_t*>(g->keys_alt.ensure(sizeof(uint64_t) * chunk_cap))
                              : nullptr;
     int* seg = static_cast<int*>(g->seg.ensure(sizeof(int) * (size_t(n) + 1)));
-    const int walk_blocks = walk_grid(g);
+    // uint32 counters are exact when this launch's visits cannot reach 2^32
+    const bool c32 = walk_variant().c32 && chunk_cap * c.length < (uint64_t(1) << 32);
+    uint32_t* counts32 = c32 ? static_cast<uint32_t*>(g->counts32.ensure(sizeof(uint32_t) * n)) : nullptr;
     float total_walk_ms = 0.f;
     for (uint64_t a = r0; a < r1; a += chunk_cap) {
         const uint64_t b = std::min(r1, a + chunk_cap);
@@ -215,13 +292,18 @@ uint64_t enqueue_campaign(saba_cu_graph* g, const saba_cu_campaign_config& c,
             walk_keys = keys_alt;
         }
         if (c.length > 1) {
+            if (c32) SABA_CUDA_CHECK(cudaMemsetAsync(counts32, 0, sizeof(uint32_t) * n, st));
             if (timing) SABA_CUDA_CHECK(cudaEventRecord(g->ev1, st));
-            walk_count_kernel<kWalksPerThread><<<walk_blocks, kWalkThreads, 0, st>>>(
-                g->d_csr, g->d_adj, walk_keys, nw, c.length, c.hash_multiplier, counts);
-            SABA_CUDA_CHECK(cudaGetLastError());
+            launch_walk(g, c32, walk_keys, nw, c.length, c.hash_multiplier,
+                        c32 ? static_cast<void*>(counts32) : static_cast<void*>(counts), st);
             ++*launches;
+            if (timing) SABA_CUDA_CHECK(cudaEventRecord(g->ev2, st));
+            if (c32) {
+                add_counts_kernel<<<g->sm_count * 4, 256, 0, st>>>(counts32, n, counts);
+                SABA_CUDA_CHECK(cudaGetLastError());
+                ++*launches;
+            }
             if (timing) {
-                SABA_CUDA_CHECK(cudaEventRecord(g->ev2, st));
                 SABA_CUDA_CHECK(cudaEventSynchronize(g->ev2));
                 float ms = 0.f;
                 SABA_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev1, g->ev2));

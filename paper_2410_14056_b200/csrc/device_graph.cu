@@ -1,4 +1,5 @@
 // K0: device CSR upload and the handle lifecycle; library identification.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -18,7 +19,64 @@ __global__ void pack_csr_kernel(const uint32_t* __restrict__ off, uint32_t n, ui
         csr[v] = make_uint2(b, off[v + 1] - b);
     }
 }
+// slot s -> word s/3, field s%3 (21 bits each)
+__global__ void pack_adj_kernel(const uint32_t* __restrict__ adj, uint64_t two_m,
+                                uint64_t* __restrict__ packed) {
+    const uint64_t words = (two_m + 2) / 3;
+    for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < words;
+         w += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t x = 0;
+        for (uint32_t r = 0; r < 3; ++r) {
+            const uint64_t s = 3 * w + r;
+            if (s < two_m) x |= uint64_t(adj[s]) << (kPackBits * r);
+        }
+        packed[w] = x;
+    }
+}
+__global__ void check_ids_kernel(const uint32_t* __restrict__ adj, uint64_t two_m, uint32_t n,
+                                 unsigned int* __restrict__ bad) {
+    uint32_t b = 0;
+    for (uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < two_m;
+         s += uint64_t(gridDim.x) * blockDim.x)
+        b |= adj[s] >= n;
+    if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
 }  // namespace
+
+void ensure_pool(int device) {
+    static bool done[64] = {};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    SABA_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    SABA_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    done[device] = true;
+}
+
+void* pool_alloc(size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    ensure_pool(dev);
+    void* p = nullptr;
+    SABA_CUDA_CHECK(cudaMallocAsync(&p, bytes, 0));
+    SABA_CUDA_CHECK(cudaStreamSynchronize(0));
+    return p;
+}
+
+void pool_free(void* p) {
+    cudaFreeAsync(p, 0);
+}
+
+const std::vector<uint32_t>& host_adj(saba_cu_graph* g) {
+    if (g->h_adj.size() != 2 * g->m) {
+        DeviceScope scope(g->device);
+        g->h_adj.resize(2 * g->m);
+        if (g->m)
+            SABA_CUDA_CHECK(cudaMemcpy(g->h_adj.data(), g->d_adj, sizeof(uint32_t) * 2 * g->m,
+                                       cudaMemcpyDeviceToHost));
+    }
+    return g->h_adj;
+}
 
 void set_last_error(const std::string& msg) { t_last_error = msg; }
 
@@ -28,7 +86,7 @@ const std::vector<uint32_t>& slot_edges(saba_cu_graph* g) {
     if (!g->h_slot_edge.empty() || g->m == 0) return g->h_slot_edge;
     // edge ids are ranks of the (u<v) pairs in sorted order (graph.hpp:92-100)
     const auto& off = g->h_off;
-    const auto& adj = g->h_adj;
+    const auto& adj = host_adj(g);
     std::vector<uint32_t> se(2 * g->m);
     uint32_t e = 0;
     for (uint32_t u = 0; u < g->n; ++u)
@@ -55,6 +113,7 @@ saba_cu_graph::~saba_cu_graph() {
     saba_cu::release_aesc_state(this);
     if (d_csr) cudaFree(d_csr);
     if (d_adj) cudaFree(d_adj);
+    if (d_adj_packed) cudaFree(d_adj_packed);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev2) cudaEventDestroy(ev2);
@@ -103,7 +162,6 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
         g->n = n;
         g->m = two_m / 2;
         g->h_off.assign(offsets, offsets + n + 1);
-        g->h_adj.assign(adjacency, adjacency + two_m);
         uint32_t dmin = UINT32_MAX, dmax = 0;
         for (uint32_t v = 0; v < n; ++v) {
             check_data(offsets[v] <= offsets[v + 1], "offsets must be nondecreasing");
@@ -111,12 +169,13 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
             dmin = d < dmin ? d : dmin;
             dmax = d > dmax ? d : dmax;
         }
-        for (uint64_t s = 0; s < two_m; ++s) check_data(adjacency[s] < n, "adjacency id out of range");
         g->min_degree = dmin;
         g->max_degree = dmax;
 
-        uint32_t* d_off = nullptr;
-        SABA_CUDA_CHECK(cudaMalloc(&d_off, sizeof(uint32_t) * (size_t(n) + 1)));
+        ensure_pool(device);
+        DevBuf d_offb, d_bad;
+        uint32_t* d_off = static_cast<uint32_t*>(d_offb.ensure(sizeof(uint32_t) * (size_t(n) + 1)));
+        unsigned int* bad = static_cast<unsigned int*>(d_bad.ensure(sizeof(unsigned int)));
         SABA_CUDA_CHECK(cudaMalloc(&g->d_csr, sizeof(uint2) * size_t(n)));
         SABA_CUDA_CHECK(cudaMalloc(&g->d_adj, sizeof(uint32_t) * (two_m ? two_m : 1)));
         SABA_CUDA_CHECK(cudaMemcpy(d_off, offsets, sizeof(uint32_t) * (size_t(n) + 1),
@@ -126,8 +185,22 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
                                        cudaMemcpyHostToDevice));
         pack_csr_kernel<<<(n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096, 256>>>(d_off, n, g->d_csr);
         SABA_CUDA_CHECK(cudaGetLastError());
+        SABA_CUDA_CHECK(cudaMemset(bad, 0, sizeof(unsigned int)));
+        check_ids_kernel<<<g->sm_count * 8, 256>>>(g->d_adj, two_m, n, bad);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        unsigned int h_bad = 0;
+        SABA_CUDA_CHECK(cudaMemcpy(&h_bad, bad, sizeof(h_bad), cudaMemcpyDeviceToHost));
+        check_data(h_bad == 0, "adjacency id out of range");
+        if (n <= kPackMax && two_m) {
+            const uint64_t words = (two_m + 2) / 3;
+            SABA_CUDA_CHECK(cudaMalloc(&g->d_adj_packed, sizeof(uint64_t) * words));
+            pack_adj_kernel<<<g->sm_count * 8, 256>>>(g->d_adj, two_m, g->d_adj_packed);
+            SABA_CUDA_CHECK(cudaGetLastError());
+        }
+        if (const char* e = getenv("SABA_L2_FETCH")) {
+            SABA_CUDA_CHECK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(atoi(e))));
+        }
         SABA_CUDA_CHECK(cudaDeviceSynchronize());
-        cudaFree(d_off);
         SABA_CUDA_CHECK(cudaEventCreate(&g->ev0));
         SABA_CUDA_CHECK(cudaEventCreate(&g->ev1));
         SABA_CUDA_CHECK(cudaEventCreate(&g->ev2));

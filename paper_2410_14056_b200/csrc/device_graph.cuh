@@ -11,6 +11,14 @@
 
 namespace saba_cu {
 
+// Stream-ordered allocations from the device's default memory pool, which is
+// configured (ensure_pool) to keep freed memory cached: workspaces of a new
+// graph handle reuse the previous handle's memory instead of paying
+// cudaMalloc/cudaFree again (this is on the end-to-end path of every call).
+void ensure_pool(int device);
+void* pool_alloc(size_t bytes);
+void pool_free(void* p);
+
 // Grow-only device buffer.
 struct DevBuf {
     void* p = nullptr;
@@ -19,14 +27,14 @@ struct DevBuf {
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) pool_free(p);
     }
     void* ensure(size_t b) {
         if (b <= bytes && p) return p;
-        if (p) cudaFree(p);
+        if (p) pool_free(p);
         p = nullptr;
         bytes = 0;
-        SABA_CUDA_CHECK(cudaMalloc(&p, b ? b : 1));
+        p = pool_alloc(b ? b : 1);
         bytes = b;
         return p;
     }
@@ -61,12 +69,16 @@ struct saba_cu_graph {
     uint64_t m = 0;
     uint32_t max_degree = 0;
     uint32_t min_degree = 0;
-    std::vector<uint32_t> h_off, h_adj;  // host CSR (graph.hpp:242-243 layout)
+    std::vector<uint32_t> h_off;         // host offsets (graph.hpp:242 layout)
+    std::vector<uint32_t> h_adj;         // host adjacency, fetched lazily (host_adj)
     std::vector<uint32_t> h_slot_edge;   // directed slot -> edge id (lazy)
     uint2* d_csr = nullptr;              // {base, degree} per vertex
     uint32_t* d_adj = nullptr;           // 2m neighbour ids, sorted per slice
+    // 3 x 21-bit ids per uint64 when n <= 2^21 (2.67 B/slot instead of 4):
+    // shrinks the random-gather working set so more of it stays in L2
+    uint64_t* d_adj_packed = nullptr;
     // campaign workspace (grow-only, reused across calls)
-    saba_cu::DevBuf kv, off, keys, keys_alt, seg, cub_tmp;
+    saba_cu::DevBuf kv, off, keys, keys_alt, seg, cub_tmp, counts32;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     saba_cu::AescState* aesc = nullptr;  // owned; freed by release_aesc_state (aesc.cu)
     ~saba_cu_graph();
@@ -74,4 +86,7 @@ struct saba_cu_graph {
 
 namespace saba_cu {
 const std::vector<uint32_t>& slot_edges(saba_cu_graph* g);
+const std::vector<uint32_t>& host_adj(saba_cu_graph* g);  // D2H once, then cached
+constexpr uint32_t kPackBits = 21;
+constexpr uint32_t kPackMax = 1u << kPackBits;  // ids must be < 2^21 to pack
 }

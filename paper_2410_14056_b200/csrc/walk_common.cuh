@@ -11,13 +11,28 @@ __device__ __forceinline__ uint2 ldg_csr(const uint2* p) { return __ldg(p); }
 __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) { return __ldg(p); }
 __device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
 
+// Neighbour id at directed slot s. Packed: 3 x 21-bit fields per uint64.
+template <bool PACKED>
+__device__ __forceinline__ uint32_t adj_at(const uint32_t* __restrict__ adj,
+                                           const uint64_t* __restrict__ packed, uint32_t s) {
+    if constexpr (PACKED) {
+        const uint32_t w = __umulhi(s, 0xAAAAAAABu) >> 1;  // s / 3 for s < 2^32
+        const uint32_t r = s - 3 * w;
+        return uint32_t(__ldg(reinterpret_cast<const unsigned long long*>(packed) + w) >> (21 * r)) &
+               0x1FFFFFu;
+    } else {
+        return __ldg(adj + s);
+    }
+}
+
 // VisitCountSink epilogue (walker.hpp:355) with warp aggregation: lanes of a
 // SABA bouquet sit on the same vertex in runs of adjacent lanes, so the head
 // of every run of equal `v` (found with one shuffle + ballot) issues a single
 // L2 reduction for the whole run. Divergent lanes degrade to one reduction
 // each. Active lanes must form a prefix of the warp; all 32 lanes must call.
-__device__ __forceinline__ void warp_count_visit(unsigned long long* __restrict__ counts, uint32_t v,
-                                                 bool act, uint32_t lane) {
+template <class CT>
+__device__ __forceinline__ void warp_count_visit(CT* __restrict__ counts, uint32_t v, bool act,
+                                                 uint32_t lane) {
     const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
     const uint32_t amask = __ballot_sync(0xffffffffu, act);
     const bool head = act && (lane == 0 || prev != v);
@@ -25,8 +40,15 @@ __device__ __forceinline__ void warp_count_visit(unsigned long long* __restrict_
     if (head) {
         const uint32_t later = heads & ~((2u << lane) - 1u);  // heads strictly above lane
         const uint32_t end = later ? uint32_t(__ffs(later) - 1) : uint32_t(__popc(amask));
-        atomicAdd(counts + v, static_cast<unsigned long long>(end - lane));
+        atomicAdd(counts + v, static_cast<CT>(end - lane));
     }
 }
 
+}  // namespace saba_cu
+
+namespace saba_cu {
+template <class CT>
+__device__ __forceinline__ void count_visit(CT* __restrict__ counts, uint32_t v, bool act) {
+    if (act) atomicAdd(counts + v, CT(1));
+}
 }  // namespace saba_cu
