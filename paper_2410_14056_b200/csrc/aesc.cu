@@ -65,6 +65,9 @@ struct AescState {
     DevBuf col_src, col_tau, degsum[2], tt, ctrl;  // per-column state
     DevBuf tau_slot, slot_edge_d, g_hat, s_hat, rho1;
     DevBuf tiles, slots, partials;
+    DevBuf heavy_rows, piece_off, pieces, part, part_mask;  // hub-row split (static per graph)
+    uint32_t nheavy = 0, npieces = 0;
+    bool heavy_built = false;
     cudaStream_t stream = nullptr;
     uint64_t* h_ctrl = nullptr;  // pinned mirror of the control block
     ~AescState() {
@@ -81,7 +84,7 @@ void release_aesc_state(saba_cu_graph* g) {
 namespace {
 
 // Control block (device): active mask, frozen-at-this-depth mask, dense flag.
-enum { kActive = 0, kFrozenNow = 1, kDense = 2, kCtrlWords = 4 };
+enum { kActive = 0, kFrozenNow = 1, kDense = 2, kDenseReq = 3, kCtrlWords = 4 };
 
 struct AescParams {
     double eps, delta, log_term;  // log_term = log(4m/delta) (aesc.hpp:109)
@@ -159,6 +162,7 @@ __global__ void aesc_init(const uint32_t* __restrict__ col_src, int ncols,
         ctrl[kActive] = ncols == 64 ? ~0ull : ((1ull << ncols) - 1);
         ctrl[kFrozenNow] = 0;
         ctrl[kDense] = 0;
+        ctrl[kDenseReq] = 0;
     }
 }
 
@@ -188,6 +192,9 @@ __global__ void aesc_check(uint32_t l, const uint32_t* __restrict__ col_src,
     if (c == 0) {
         ctrl[kFrozenNow] = frozen;
         ctrl[kActive] = active & ~frozen;
+        // dense mode switches only between depths, so every kernel of one
+        // depth sees the same mode
+        if (ctrl[kDenseReq]) ctrl[kDense] = 1;
     }
 }
 
@@ -244,8 +251,70 @@ __global__ void aesc_expand(const uint2* __restrict__ csr, const uint32_t* __res
     }
 }
 
-// Pull SpMM over the candidate rows (sparse) or all rows (dense). Warp per
-// row, lane = columns {2 lane, 2 lane + 1}; neighbours in ascending order.
+// Rows with more than kHeavy neighbours are split into fixed pieces of
+// kHeavy neighbours (warp per piece) whose partial sums are combined in piece
+// order: a deterministic function of the row alone, and no hub row sits on
+// one warp's critical path.
+constexpr uint32_t kHeavy = 256;
+
+// Sum of Q rows (2 columns per lane) and OR of support masks over the
+// neighbour slots [b, e), in slot order; 8 gathers in flight per warp.
+__device__ __forceinline__ void pull_range(const uint32_t* __restrict__ adj,
+                                           const double* __restrict__ Qc,
+                                           const unsigned long long* __restrict__ Mc, uint32_t b,
+                                           uint32_t e, uint32_t lane, double& a0, double& a1,
+                                           unsigned long long& mask) {
+    for (uint32_t s0 = b; s0 < e; s0 += 32) {
+        const uint32_t cnt = min(32u, e - s0);
+        const uint32_t mine = lane < cnt ? adj[s0 + lane] : 0u;
+        uint32_t k = 0;
+        for (; k + 8 <= cnt; k += 8) {
+            double2 q[8];
+            unsigned long long mm[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t v = __shfl_sync(0xffffffffu, mine, k + j);
+                mm[j] = Mc[v];
+                q[j] = reinterpret_cast<const double2*>(Qc + size_t(v) * kCols)[lane];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                mask |= mm[j];
+                a0 += q[j].x;
+                a1 += q[j].y;
+            }
+        }
+        for (; k < cnt; ++k) {
+            const uint32_t v = __shfl_sync(0xffffffffu, mine, k);
+            mask |= Mc[v];
+            const double2 q = reinterpret_cast<const double2*>(Qc + size_t(v) * kCols)[lane];
+            a0 += q.x;
+            a1 += q.y;
+        }
+    }
+}
+
+// Write one finished row of depth l+1 (P, Q = P / d, support mask) and
+// account its degree into the support degree sums of its columns.
+__device__ __forceinline__ void pull_store(uint32_t x, uint32_t deg, double a0, double a1,
+                                           unsigned long long mask, unsigned long long active,
+                                           uint32_t lane, double* __restrict__ Pn,
+                                           double* __restrict__ Qn, unsigned long long* __restrict__ Mn,
+                                           unsigned long long& ds0, unsigned long long& ds1) {
+    const unsigned long long lo_mask = 1ull << (2 * lane), hi_mask = 1ull << (2 * lane + 1);
+    mask &= active;
+    if (!(active & lo_mask)) a0 = 0.0;
+    if (!(active & hi_mask)) a1 = 0.0;
+    const double dx = double(deg);
+    reinterpret_cast<double2*>(Pn + size_t(x) * kCols)[lane] = make_double2(a0, a1);
+    reinterpret_cast<double2*>(Qn + size_t(x) * kCols)[lane] = make_double2(a0 / dx, a1 / dx);
+    if (lane == 0) Mn[x] = mask;
+    if (mask & lo_mask) ds0 += deg;
+    if (mask & hi_mask) ds1 += deg;
+}
+
+// Pull SpMM over the candidate rows (sparse) or all rows (dense) with at
+// most kHeavy neighbours. Warp per row, lane = columns {2 lane, 2 lane + 1}.
 __global__ void __launch_bounds__(256)
     aesc_pull(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
               const double* __restrict__ Qc, const unsigned long long* __restrict__ Mc,
@@ -258,43 +327,83 @@ __global__ void __launch_bounds__(256)
     const bool dense = ctrl[kDense] != 0;
     const uint32_t rows = dense ? n : *ucount_next;
     const uint32_t lane = threadIdx.x & 31;
-    const unsigned long long lo_mask = 1ull << (2 * lane), hi_mask = 1ull << (2 * lane + 1);
-    const bool act0 = (active & lo_mask) != 0, act1 = (active & hi_mask) != 0;
     unsigned long long ds0 = 0, ds1 = 0;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < rows;
          i += (gridDim.x * blockDim.x) >> 5) {
         const uint32_t x = dense ? i : ulist_next[i];
         const uint2 r = csr[x];
+        if (r.y > kHeavy) continue;  // pieces + combine
         double a0 = 0.0, a1 = 0.0;
         unsigned long long mask = 0;
-        for (uint32_t s0 = r.x; s0 < r.x + r.y; s0 += 32) {
-            const uint32_t cnt = min(32u, r.x + r.y - s0);
-            const uint32_t mine = lane < cnt ? adj[s0 + lane] : 0u;
-            for (uint32_t k = 0; k < cnt; ++k) {
-                const uint32_t v = __shfl_sync(0xffffffffu, mine, k);
-                mask |= Mc[v];
-                const double2 q = reinterpret_cast<const double2*>(Qc + size_t(v) * kCols)[lane];
-                a0 += q.x;
-                a1 += q.y;
-            }
-        }
-        mask &= active;
-        if (!act0) a0 = 0.0;
-        if (!act1) a1 = 0.0;
-        const double dx = double(r.y);
-        reinterpret_cast<double2*>(Pn + size_t(x) * kCols)[lane] = make_double2(a0, a1);
-        reinterpret_cast<double2*>(Qn + size_t(x) * kCols)[lane] = make_double2(a0 / dx, a1 / dx);
-        if (lane == 0) {
-            Mn[x] = mask;
-            if (!dense) flag[x] = 0;
-        }
-        if (mask & lo_mask) ds0 += r.y;
-        if (mask & hi_mask) ds1 += r.y;
+        pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, a0, a1, mask);
+        pull_store(x, r.y, a0, a1, mask, active, lane, Pn, Qn, Mn, ds0, ds1);
+        if (lane == 0 && !dense) flag[x] = 0;
     }
     if (ds0) atomicAdd(degsum_next + 2 * lane, ds0);  // integer: order-free
     if (ds1) atomicAdd(degsum_next + 2 * lane + 1, ds1);
     // switch to dense rows once the frontier covers a quarter of the graph
-    if (!dense && blockIdx.x == 0 && threadIdx.x == 0 && rows > n / 4) ctrl[kDense] = 1;
+    if (!dense && blockIdx.x == 0 && threadIdx.x == 0 && rows > n / 4) ctrl[kDenseReq] = 1;
+}
+
+struct HeavyPiece {
+    uint32_t row, begin, end, pad;
+};
+
+// Warp per piece of a heavy row that is a candidate at this depth.
+__global__ void __launch_bounds__(256)
+    aesc_pull_pieces(const HeavyPiece* __restrict__ pieces, uint32_t npieces,
+                     const uint32_t* __restrict__ adj, const double* __restrict__ Qc,
+                     const unsigned long long* __restrict__ Mc, const uint32_t* __restrict__ flag,
+                     double* __restrict__ part, unsigned long long* __restrict__ part_mask,
+                     const unsigned long long* __restrict__ ctrl) {
+    if (!ctrl[kActive]) return;
+    const bool dense = ctrl[kDense] != 0;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < npieces;
+         i += (gridDim.x * blockDim.x) >> 5) {
+        const HeavyPiece pc = pieces[i];
+        if (!dense && !flag[pc.row]) continue;
+        double a0 = 0.0, a1 = 0.0;
+        unsigned long long mask = 0;
+        pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, a0, a1, mask);
+        reinterpret_cast<double2*>(part + size_t(i) * kCols)[lane] = make_double2(a0, a1);
+        if (lane == 0) part_mask[i] = mask;
+    }
+}
+
+// Warp per heavy row: fold its pieces in order and store the row.
+__global__ void aesc_pull_combine(const uint32_t* __restrict__ heavy_rows,
+                                  const uint32_t* __restrict__ piece_off, uint32_t nheavy,
+                                  const uint2* __restrict__ csr, const double* __restrict__ part,
+                                  const unsigned long long* __restrict__ part_mask,
+                                  double* __restrict__ Pn, double* __restrict__ Qn,
+                                  unsigned long long* __restrict__ Mn, uint32_t* __restrict__ flag,
+                                  unsigned long long* __restrict__ degsum_next,
+                                  const unsigned long long* __restrict__ ctrl) {
+    const unsigned long long active = ctrl[kActive];
+    if (!active) return;
+    const bool dense = ctrl[kDense] != 0;
+    const uint32_t lane = threadIdx.x & 31;
+    unsigned long long ds0 = 0, ds1 = 0;
+    for (uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; h < nheavy;
+         h += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t x = heavy_rows[h];
+        if (!dense && !flag[x]) continue;
+        const uint32_t p0 = piece_off[h], p1 = piece_off[h + 1];
+        double2 a = reinterpret_cast<const double2*>(part + size_t(p0) * kCols)[lane];
+        unsigned long long mask = part_mask[p0];
+        for (uint32_t p = p0 + 1; p < p1; ++p) {
+            const double2 b = reinterpret_cast<const double2*>(part + size_t(p) * kCols)[lane];
+            a.x += b.x;
+            a.y += b.y;
+            mask |= part_mask[p];
+        }
+        pull_store(x, csr[x].y, a.x, a.y, mask, active, lane, Pn, Qn, Mn, ds0, ds1);
+        __syncwarp();
+        if (lane == 0 && !dense) flag[x] = 0;
+    }
+    if (ds0) atomicAdd(degsum_next + 2 * lane, ds0);
+    if (ds1) atomicAdd(degsum_next + 2 * lane + 1, ds1);
 }
 
 // Hook (aesc.hpp:581-588) at depth l+1 for the columns that just stepped.
@@ -500,6 +609,7 @@ struct Engine {
             buf<uint32_t>(st->tlist, n);
             st->n_cap = n;
         }
+        if (!st->heavy_built) build_heavy();
         buf<uint32_t>(st->ucount, 2);
         buf<uint32_t>(st->tcount, 1);
         buf<uint32_t>(st->col_src, kCols);
@@ -508,6 +618,31 @@ struct Engine {
         buf<uint64_t>(st->degsum[1], kCols);
         buf<uint32_t>(st->tt, kCols);
         buf<uint64_t>(st->ctrl, kCtrlWords);
+    }
+
+    // Rows with degree > kHeavy and their fixed pieces of kHeavy neighbours.
+    void build_heavy() {
+        std::vector<uint32_t> rows, poff{0};
+        std::vector<HeavyPiece> pcs;
+        for (uint32_t v = 0; v < g->n; ++v) {
+            const uint32_t b = g->h_off[v], e = g->h_off[v + 1];
+            if (e - b <= kHeavy) continue;
+            rows.push_back(v);
+            for (uint32_t s = b; s < e; s += kHeavy) pcs.push_back({v, s, std::min(e, s + kHeavy), 0});
+            poff.push_back(uint32_t(pcs.size()));
+        }
+        st->nheavy = uint32_t(rows.size());
+        st->npieces = uint32_t(pcs.size());
+        SABA_CUDA_CHECK(cudaMemcpyAsync(buf<uint32_t>(st->heavy_rows, rows.size()), rows.data(),
+                                        sizeof(uint32_t) * rows.size(), cudaMemcpyHostToDevice, s));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(buf<uint32_t>(st->piece_off, poff.size()), poff.data(),
+                                        sizeof(uint32_t) * poff.size(), cudaMemcpyHostToDevice, s));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(buf<HeavyPiece>(st->pieces, pcs.size()), pcs.data(),
+                                        sizeof(HeavyPiece) * pcs.size(), cudaMemcpyHostToDevice, s));
+        buf<double>(st->part, size_t(pcs.size()) * kCols);
+        buf<uint64_t>(st->part_mask, pcs.size());
+        SABA_CUDA_CHECK(cudaStreamSynchronize(s));  // host vectors go out of scope
+        st->heavy_built = true;
     }
 
     void upload_tau(std::vector<uint32_t> ts) {
@@ -575,6 +710,16 @@ struct Engine {
             SABA_CUDA_CHECK(cudaMemsetAsync(UC + (cur ^ 1), 0, sizeof(uint32_t), s));
             aesc_expand<<<grid, 256, 0, s>>>(csr, adj, M[cur], UL[cur], UC + cur, UL[cur ^ 1],
                                              UC + (cur ^ 1), flag, tflag, tlist, tcount, ctrl);
+            if (st->npieces) {
+                aesc_pull_pieces<<<grid, 256, 0, s>>>(st->pieces.as<HeavyPiece>(), st->npieces, adj,
+                                                      Q[cur], M[cur], flag, st->part.as<double>(),
+                                                      st->part_mask.as<unsigned long long>(), ctrl);
+                aesc_pull_combine<<<grid, 256, 0, s>>>(
+                    st->heavy_rows.as<uint32_t>(), st->piece_off.as<uint32_t>(), st->nheavy, csr,
+                    st->part.as<double>(), st->part_mask.as<unsigned long long>(), P[cur ^ 1],
+                    Q[cur ^ 1], M[cur ^ 1], flag, DS[cur ^ 1], ctrl);
+                launches += 2;
+            }
             aesc_pull<<<grid, 256, 0, s>>>(csr, adj, Q[cur], M[cur], P[cur ^ 1], Q[cur ^ 1], M[cur ^ 1],
                                            UL[cur ^ 1], UC + (cur ^ 1), flag, DS[cur ^ 1], ctrl, n);
             aesc_hook<<<nc, 128, 0, s>>>(l + 1, st->col_src.as<uint32_t>(), csr, adj, tsl, P[cur ^ 1],

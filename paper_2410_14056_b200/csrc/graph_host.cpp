@@ -287,9 +287,21 @@ int saba_gen_chung_lu(uint32_t n, double gamma, double mean_degree, double max_d
 #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < int64_t(n); ++i)
             w[size_t(i)] = std::pow(1.0 - unit53(counter_hash(s, uint64_t(i))), ex);
-        double sum = 0.0;
-        for (double x : w) sum += x;
-        const double scalef = mean_degree * double(n) / sum;
+        // scale c such that the mean of the CAPPED weights min(c w, cap) is
+        // mean_degree (capping removes tail mass; bisection, deterministic)
+        auto capped_mean = [&](double c) {
+            double s = 0.0;
+            for (double x : w) s += std::min(x * c, max_degree);
+            return s / double(n);
+        };
+        double lo = 0.0, hi = 1.0;
+        while (capped_mean(hi) < mean_degree && hi < 1e30) hi *= 2.0;
+        check_arg(capped_mean(hi) >= mean_degree, "chung_lu: mean_degree unreachable under the cap");
+        for (int it = 0; it < 100; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            (capped_mean(mid) < mean_degree ? lo : hi) = mid;
+        }
+        const double scalef = hi;
         double total = 0.0;
         for (double& x : w) {
             x = std::min(x * scalef, max_degree);

@@ -91,9 +91,16 @@ double host_estimate_decay(const HostCsr& g, uint32_t iters, bool bip, const std
     if (nx < 1e-12) return 0.0;
     for (double& t : x) t /= nx;
     double lambda = 0.0;
+    // Element-wise passes and the SpMV rows are independent, so they run in
+    // parallel with each element computed exactly as the reference does
+    // (row sums in neighbour order); the three reductions (two projections,
+    // the norm) stay sequential, so lambda_hat is bit-identical.
+    const int64_t N = n;
     for (uint32_t it = 0; it < iters; ++it) {
-        for (uint32_t v = 0; v < n; ++v) z[v] = x[v] * isd[v];
-        for (uint32_t u = 0; u < n; ++u) {
+#pragma omp parallel for schedule(static)
+        for (int64_t v = 0; v < N; ++v) z[v] = x[v] * isd[v];
+#pragma omp parallel for schedule(dynamic, 1024)
+        for (int64_t u = 0; u < N; ++u) {
             double acc = 0.0;
             for (uint32_t s = g.off[u]; s < g.off[u + 1]; ++s) acc += z[g.adj[s]];
             y[u] = acc * isd[u];
@@ -102,7 +109,8 @@ double host_estimate_decay(const HostCsr& g, uint32_t iters, bool bip, const std
         const double ny = norm(y);
         if (ny < 1e-15) return 0.0;
         lambda = ny;
-        for (uint32_t v = 0; v < n; ++v) x[v] = y[v] / ny;
+#pragma omp parallel for schedule(static)
+        for (int64_t v = 0; v < N; ++v) x[v] = y[v] / ny;
     }
     return std::min(lambda, 1.0);
 }
