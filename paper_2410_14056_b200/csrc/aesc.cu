@@ -40,6 +40,7 @@
 // support(l)), and aesc_clear restores it between batches.
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_reduce.cuh>
+#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -54,9 +55,6 @@
 namespace saba_cu {
 
 constexpr int kCols = 64;           // sources per propagation batch
-constexpr int kTileThreads = 256;   // walk-phase block
-constexpr int kTileIPT = 8;         // walks per thread per side
-constexpr int kTile = kTileThreads * kTileIPT;  // pair indices per tile
 
 struct AescState {
     uint32_t n_cap = 0;
@@ -64,7 +62,7 @@ struct AescState {
     DevBuf ulist[2], ucount, flag, tflag, tlist, tcount;
     DevBuf col_src, col_tau, degsum[2], tt, ctrl;  // per-column state
     DevBuf tau_slot, slot_edge_d, g_hat, s_hat, rho1;
-    DevBuf tiles, slots, partials;
+    DevBuf tiles, slots, partials, groups, woffs, keys[2], vals[2], score, sort_tmp;
     DevBuf heavy_rows, piece_off, pieces, part, part_mask;  // hub-row split (static per graph)
     uint32_t nheavy = 0, npieces = 0;
     bool heavy_built = false;
@@ -447,96 +445,141 @@ __global__ void aesc_clear(const uint32_t* __restrict__ tlist, const uint32_t* _
     }
 }
 
-struct WalkTile {
-    uint64_t k0;         // first pair index of the tile
+// Walk phase layout. A slot's n_req pairs are split into groups of at most
+// kGroupPairs pairs; a chunk holds whole groups (<= kChunkWalks walks, both
+// sides). Within a chunk every walk gets the key (group << 16 | seed >> 16)
+// and one radix sort orders the chunk by group then seed: a warp then walks
+// 32 adjacent seeds of one (slot, side) — the SABA bouquet over the slot's
+// whole seed set, not just a tile (PAPER Alg. 3 + §3.3; walker.hpp:436-439).
+constexpr uint32_t kGroupPairs = 1u << 24;
+constexpr uint32_t kSeedBits = 16;
+constexpr uint64_t kChunkWalks = uint64_t(1) << 28;
+constexpr uint32_t kPairTile = 2048;  // pairs per deterministic reduction tile
+
+struct WalkGroup {
     uint64_t edge_seed;  // substream(src_seed, slot) (aesc.hpp:622)
-    double inv_n;        // 1 / n_req (aesc.hpp:512)
-    uint32_t vi, vj;     // side 0 / side 1 start vertices
-    uint32_t count;      // pairs in this tile (<= kTile)
-    uint32_t len;        // tau_eff + 1
+    uint64_t k0;         // first pair index of the group within its slot
+    uint32_t pairs;      // pairs in this group
+    uint32_t walk_off;   // side-0 walks at [walk_off, +pairs), side 1 after them
+    uint32_t vi, vj;     // side 0 / side 1 start vertices (aesc.hpp:518-521)
+    uint32_t len;        // tau_eff + 1 vertices
     uint32_t col;        // rho column
-    uint32_t pad;
+};
+
+struct PairTile {
+    double inv_n;  // 1 / n_req (aesc.hpp:512)
+    uint32_t group, p0, count, out;
 };
 
 struct SlotWork {
-    uint32_t t0, t1;  // tile range
+    uint32_t t0, t1;  // global tile range of the slot, in pair order
     uint32_t slot;    // directed slot receiving the estimate
     uint32_t pad;
 };
 
-// K4: one tile per block iteration (persistent grid-stride).
-template <bool PACKED>
-__global__ void __launch_bounds__(kTileThreads)
-    aesc_walk(const WalkTile* __restrict__ tiles, uint32_t ntiles, const uint2* __restrict__ csr,
-              const uint32_t* __restrict__ adj, const uint64_t* __restrict__ adjp,
-              const double* __restrict__ R, uint32_t n, uint64_t mult,
-              double* __restrict__ partials) {
-    using Sort = cub::BlockRadixSort<uint32_t, kTileThreads, kTileIPT, uint32_t>;
-    using Reduce = cub::BlockReduce<double, kTileThreads, cub::BLOCK_REDUCE_WARP_REDUCTIONS>;
-    __shared__ union {
-        typename Sort::TempStorage sort;
-        double score1[kTile];
-        typename Reduce::TempStorage reduce;
-    } sm;
-    __shared__ double score0[kTile];
-    const uint32_t tid = threadIdx.x;
-    for (uint32_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-        const WalkTile t = tiles[ti];
-        const double* rho = R + size_t(t.col) * n;
-        const uint32_t groups = (t.count + kTileThreads - 1) / kTileThreads;  // block-uniform
-        for (uint32_t side = 0; side < 2; ++side) {
-            uint32_t key[kTileIPT], item[kTileIPT];
-#pragma unroll
-            for (int i = 0; i < kTileIPT; ++i) {
-                const uint32_t it = tid * kTileIPT + i;
-                item[i] = it < t.count ? it : 0xffffffffu;
-                // walk seed counter_hash(edge_seed, 2k+side) >> 32 (aesc.hpp:485)
-                key[i] = it < t.count ? walk_seed(t.edge_seed, 2 * (t.k0 + it) + side) : 0xffffffffu;
-            }
-            // SABA: sort the tile's seeds so a warp holds 32 adjacent seeds
-            // (the top 16 bits decide the bouquet clustering; the order never
-            // affects a score)
-            __syncthreads();
-            Sort(sm.sort).SortBlockedToStriped(key, item, 16, 32);
-            __syncthreads();
-            const uint32_t start = side ? t.vj : t.vi;
-            uint32_t cur[kTileIPT];
-            double sc[kTileIPT];
-#pragma unroll
-            for (int i = 0; i < kTileIPT; ++i) {
-                cur[i] = start;
-                sc[i] = 0.0;
-            }
-            for (uint32_t l = 1; l < t.len; ++l) {
-                uint2 rec[kTileIPT];
-#pragma unroll
-                for (int i = 0; i < kTileIPT; ++i)
-                    if (i < groups) rec[i] = ldg_csr(csr + cur[i]);
-#pragma unroll
-                for (int i = 0; i < kTileIPT; ++i)
-                    if (i < groups) {
-                        const uint32_t raw = key[i] ^ hash_state(mult, cur[i], l);
-                        cur[i] = adj_at<PACKED>(adj, adjp, rec[i].x + scaled_index(raw, rec[i].y));
-                    }
-#pragma unroll
-                for (int i = 0; i < kTileIPT; ++i)
-                    if (i < groups) sc[i] += __ldg(rho + cur[i]);  // step order (aesc.hpp:492)
-            }
-            double* dst = side ? sm.score1 : score0;
-#pragma unroll
-            for (int i = 0; i < kTileIPT; ++i)
-                if (item[i] != 0xffffffffu) dst[item[i]] = sc[i];
-            __syncthreads();
+__global__ void aesc_keygen(const WalkGroup* __restrict__ groups, const uint32_t* __restrict__ walk_offs,
+                            uint32_t ngroups, uint32_t nwalks, uint32_t* __restrict__ keys,
+                            uint32_t* __restrict__ vals) {
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwalks; w += gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = ngroups;  // walk_offs[g] <= w < walk_offs[g+1]
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (walk_offs[mid] <= w) lo = mid; else hi = mid;
         }
+        const WalkGroup G = groups[lo];
+        const uint32_t local = w - G.walk_off;
+        const uint32_t side = local >= G.pairs;
+        const uint64_t k = G.k0 + (local - side * G.pairs);
+        // walk seed counter_hash(edge_seed, 2k+side) >> 32 (aesc.hpp:485)
+        const uint32_t seed = walk_seed(G.edge_seed, 2 * k + side);
+        keys[w] = (lo << kSeedBits) | (seed >> (32 - kSeedBits));
+        vals[w] = w;
+    }
+}
+
+// K4: warps walk consecutive sorted entries (WPT per lane); the score of
+// walk w = sum of rho over steps 1..len-1 in step order (aesc.hpp:491-493).
+template <bool PACKED, int WPT>
+__global__ void __launch_bounds__(256)
+    aesc_walk_sorted(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                     uint32_t nwalks, const WalkGroup* __restrict__ groups,
+                     const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                     const uint64_t* __restrict__ adjp, const double* __restrict__ R, uint32_t n,
+                     uint64_t mult, double* __restrict__ score) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint64_t base = uint64_t(warp) * 32 * WPT; base < nwalks; base += uint64_t(nwarps) * 32 * WPT) {
+        uint32_t cur[WPT], seed[WPT], len[WPT], w[WPT];
+        const double* rho[WPT];
+        double sc[WPT];
+        uint32_t maxlen = 1;
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {
+            const uint64_t e = base + uint64_t(r) * 32 + lane;
+            len[r] = 1;
+            sc[r] = 0.0;
+            w[r] = 0xffffffffu;
+            cur[r] = 0;
+            seed[r] = 0;
+            rho[r] = R;
+            if (e < nwalks) {
+                w[r] = vals[e];
+                const WalkGroup G = groups[keys[e] >> kSeedBits];
+                const uint32_t local = w[r] - G.walk_off;
+                const uint32_t side = local >= G.pairs;
+                seed[r] = walk_seed(G.edge_seed, 2 * (G.k0 + (local - side * G.pairs)) + side);
+                cur[r] = side ? G.vj : G.vi;
+                len[r] = G.len;
+                rho[r] = R + size_t(G.col) * n;
+            }
+            maxlen = max(maxlen, len[r]);
+        }
+        maxlen = __reduce_max_sync(0xffffffffu, maxlen);
+        for (uint32_t l = 1; l < maxlen; ++l) {
+            uint2 rec[WPT];
+#pragma unroll
+            for (int r = 0; r < WPT; ++r)
+                if (l < len[r]) rec[r] = ldg_csr(csr + cur[r]);
+#pragma unroll
+            for (int r = 0; r < WPT; ++r)
+                if (l < len[r]) {
+                    const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
+                    cur[r] = adj_at<PACKED>(adj, adjp, rec[r].x + scaled_index(raw, rec[r].y));
+                }
+#pragma unroll
+            for (int r = 0; r < WPT; ++r)
+                if (l < len[r]) sc[r] += __ldg(rho[r] + cur[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < WPT; ++r)
+            if (w[r] != 0xffffffffu) score[w[r]] = sc[r];
+    }
+}
+
+// (a_k - b_k) / n_req over a tile of pair indices, thread-sequential then a
+// fixed block tree (aesc.hpp:522 folds left; only the order differs).
+__global__ void __launch_bounds__(256)
+    aesc_pair_reduce(const PairTile* __restrict__ tiles, uint32_t ntiles,
+                     const WalkGroup* __restrict__ groups, const double* __restrict__ score,
+                     double* __restrict__ partials) {
+    using Reduce = cub::BlockReduce<double, 256, cub::BLOCK_REDUCE_WARP_REDUCTIONS>;
+    __shared__ typename Reduce::TempStorage tmp;
+    constexpr uint32_t IPT = kPairTile / 256;
+    for (uint32_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        const PairTile T = tiles[ti];
+        const WalkGroup G = groups[T.group];
         double x = 0.0;
 #pragma unroll
-        for (int i = 0; i < kTileIPT; ++i) {
-            const uint32_t it = tid * kTileIPT + i;
-            if (it < t.count) x += (score0[it] - sm.score1[it]) * t.inv_n;  // aesc.hpp:522
+        for (uint32_t i = 0; i < IPT; ++i) {
+            const uint32_t p = threadIdx.x * IPT + i;
+            if (p < T.count) {
+                const uint32_t k = G.walk_off + T.p0 + p;
+                x += (score[k] - score[k + G.pairs]) * T.inv_n;
+            }
         }
-        __syncthreads();  // score1 aliases the reduce storage
-        const double tot = Reduce(sm.reduce).Sum(x);
-        if (tid == 0) partials[ti] = tot;
+        const double tot = Reduce(tmp).Sum(x);
+        if (threadIdx.x == 0) partials[T.out] = tot;
         __syncthreads();
     }
 }
@@ -769,60 +812,108 @@ void validate_cfg(const saba_cu_aesc_config& c) {
               "aesc: mode not supported on GPU (naive/vector-mod are CPU LCG baselines)");
 }
 
+// Host plan of one walk phase: slots -> groups -> chunks, tiles in pair order.
 struct TileBuilder {
-    std::vector<WalkTile> tiles;
+    struct Chunk {
+        std::vector<WalkGroup> groups;
+        std::vector<uint32_t> offs;  // walk offsets + sentinel
+        std::vector<PairTile> tiles;
+        uint32_t walks = 0;
+    };
+    std::vector<Chunk> chunks;
     std::vector<SlotWork> slots;
+    uint32_t ntiles = 0;
+
+    void clear() {
+        chunks.clear();
+        slots.clear();
+        ntiles = 0;
+    }
+    bool empty() const { return slots.empty(); }
+
     void add(uint32_t slot, uint32_t vi, uint32_t vj, uint32_t len, uint64_t n_req, uint64_t edge_seed,
              uint32_t col) {
-        SlotWork w{uint32_t(tiles.size()), 0, slot, 0};
+        SlotWork w{ntiles, 0, slot, 0};
         const double inv_n = 1.0 / double(n_req);
-        for (uint64_t k0 = 0; k0 < n_req; k0 += kTile) {
-            WalkTile t{};
-            t.k0 = k0;
-            t.edge_seed = edge_seed;
-            t.inv_n = inv_n;
-            t.vi = vi;
-            t.vj = vj;
-            t.count = uint32_t(std::min<uint64_t>(kTile, n_req - k0));
-            t.len = len;
-            t.col = col;
-            tiles.push_back(t);
+        for (uint64_t k0 = 0; k0 < n_req; k0 += kGroupPairs) {
+            const uint32_t pairs = uint32_t(std::min<uint64_t>(kGroupPairs, n_req - k0));
+            if (chunks.empty() || chunks.back().walks + 2ull * pairs > kChunkWalks ||
+                chunks.back().groups.size() >= (1u << (32 - kSeedBits)))
+                chunks.emplace_back();
+            Chunk& c = chunks.back();
+            const uint32_t gi = uint32_t(c.groups.size());
+            c.groups.push_back({edge_seed, k0, pairs, c.walks, vi, vj, len, col});
+            c.offs.push_back(c.walks);
+            for (uint32_t p0 = 0; p0 < pairs; p0 += kPairTile)
+                c.tiles.push_back({inv_n, gi, p0, std::min(kPairTile, pairs - p0), ntiles++});
+            c.walks += 2 * pairs;
         }
-        w.t1 = uint32_t(tiles.size());
+        w.t1 = ntiles;
         slots.push_back(w);
     }
 };
 
-void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, const TileBuilder& tb,
-               const double* R, uint64_t mult, double* g_hat_dev, uint32_t* launches) {
-    if (tb.tiles.empty()) return;
-    WalkTile* dt = static_cast<WalkTile*>(st->tiles.ensure(sizeof(WalkTile) * tb.tiles.size()));
-    SlotWork* ds = static_cast<SlotWork*>(st->slots.ensure(sizeof(SlotWork) * tb.slots.size()));
-    double* part = static_cast<double*>(st->partials.ensure(sizeof(double) * tb.tiles.size()));
-    SABA_CUDA_CHECK(cudaMemcpyAsync(dt, tb.tiles.data(), sizeof(WalkTile) * tb.tiles.size(),
-                                    cudaMemcpyHostToDevice, s));
-    SABA_CUDA_CHECK(cudaMemcpyAsync(ds, tb.slots.data(), sizeof(SlotWork) * tb.slots.size(),
-                                    cudaMemcpyHostToDevice, s));
+int bits_for(uint32_t x) {
+    int b = 0;
+    while ((1ull << b) < x) ++b;
+    return b;
+}
+
+// Walk phase: per chunk keygen -> radix sort (group, seed top bits) -> sorted
+// walks -> pair tiles; then the per-slot fold into g_hat.
+void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb, const double* R,
+               uint64_t mult, double* g_hat_dev, uint32_t* launches) {
+    if (tb.empty()) return;
+    double* part = static_cast<double*>(st->partials.ensure(sizeof(double) * std::max(tb.ntiles, 1u)));
     const bool packed = g->d_adj_packed != nullptr;
+    constexpr int WPT = 4;
     int occ = 0;
     if (packed)
-        SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk<true>, kTileThreads, 0));
+        SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk_sorted<true, WPT>, 256, 0));
     else
-        SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk<false>, kTileThreads, 0));
-    const uint32_t nt = uint32_t(tb.tiles.size());
-    const int grid = int(std::min<uint64_t>(nt, uint64_t(g->sm_count) * std::max(occ, 1)));
-    if (packed)
-        aesc_walk<true><<<grid, kTileThreads, 0, s>>>(dt, nt, g->d_csr, g->d_adj, g->d_adj_packed, R,
-                                                      g->n, mult, part);
-    else
-        aesc_walk<false><<<grid, kTileThreads, 0, s>>>(dt, nt, g->d_csr, g->d_adj, g->d_adj_packed, R,
-                                                       g->n, mult, part);
-    SABA_CUDA_CHECK(cudaGetLastError());
+        SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk_sorted<false, WPT>, 256, 0));
+    for (TileBuilder::Chunk& c : tb.chunks) {
+        const uint32_t ng = uint32_t(c.groups.size()), nw = c.walks, nt = uint32_t(c.tiles.size());
+        c.offs.push_back(nw);
+        auto* dg = static_cast<WalkGroup*>(st->groups.ensure(sizeof(WalkGroup) * ng));
+        auto* doff = static_cast<uint32_t*>(st->woffs.ensure(sizeof(uint32_t) * (ng + 1)));
+        auto* dt = static_cast<PairTile*>(st->tiles.ensure(sizeof(PairTile) * nt));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(dg, c.groups.data(), sizeof(WalkGroup) * ng, cudaMemcpyHostToDevice, s));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(doff, c.offs.data(), sizeof(uint32_t) * (ng + 1), cudaMemcpyHostToDevice, s));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(dt, c.tiles.data(), sizeof(PairTile) * nt, cudaMemcpyHostToDevice, s));
+        cub::DoubleBuffer<uint32_t> keys(static_cast<uint32_t*>(st->keys[0].ensure(sizeof(uint32_t) * nw)),
+                                         static_cast<uint32_t*>(st->keys[1].ensure(sizeof(uint32_t) * nw)));
+        cub::DoubleBuffer<uint32_t> vals(static_cast<uint32_t*>(st->vals[0].ensure(sizeof(uint32_t) * nw)),
+                                         static_cast<uint32_t*>(st->vals[1].ensure(sizeof(uint32_t) * nw)));
+        double* score = static_cast<double*>(st->score.ensure(sizeof(double) * nw));
+        aesc_keygen<<<g->sm_count * 8, 256, 0, s>>>(dg, doff, ng, nw, keys.Current(), vals.Current());
+        SABA_CUDA_CHECK(cudaGetLastError());
+        const int end_bit = int(kSeedBits) + std::max(1, bits_for(ng));
+        size_t tmp = 0;
+        SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, int(nw), 0, end_bit, s));
+        void* t = st->sort_tmp.ensure(tmp);
+        SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(t, tmp, keys, vals, int(nw), 0, end_bit, s));
+        const int grid = int(std::min<uint64_t>((nw + 32 * WPT - 1) / (32 * WPT) * 32 / 256 + 1,
+                                                uint64_t(g->sm_count) * std::max(occ, 1)));
+        if (packed)
+            aesc_walk_sorted<true, WPT><<<grid, 256, 0, s>>>(keys.Current(), vals.Current(), nw, dg, g->d_csr,
+                                                             g->d_adj, g->d_adj_packed, R, g->n, mult, score);
+        else
+            aesc_walk_sorted<false, WPT><<<grid, 256, 0, s>>>(keys.Current(), vals.Current(), nw, dg, g->d_csr,
+                                                              g->d_adj, g->d_adj_packed, R, g->n, mult, score);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        aesc_pair_reduce<<<int(std::min<uint32_t>(nt, g->sm_count * 8)), 256, 0, s>>>(dt, nt, dg, score, part);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        *launches += 4;
+        // the chunk's host metadata must outlive its uploads
+        SABA_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
     const uint32_t nsw = uint32_t(tb.slots.size());
+    auto* ds = static_cast<SlotWork*>(st->slots.ensure(sizeof(SlotWork) * nsw));
+    SABA_CUDA_CHECK(cudaMemcpyAsync(ds, tb.slots.data(), sizeof(SlotWork) * nsw, cudaMemcpyHostToDevice, s));
     aesc_slot_reduce<<<(nsw + 127) / 128, 128, 0, s>>>(ds, nsw, part, g_hat_dev);
     SABA_CUDA_CHECK(cudaGetLastError());
-    *launches += 2;
-    // the host tile vectors are reused by the caller: finish the uploads first
+    ++*launches;
     SABA_CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
@@ -913,8 +1004,7 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
             SABA_CUDA_CHECK(cudaEventRecord(e0, E.s));
             const std::vector<uint32_t> tt = E.propagate(cols, d_g);
             SABA_CUDA_CHECK(cudaEventRecord(e1, E.s));
-            tb.tiles.clear();
-            tb.slots.clear();
+            tb.clear();
             for (size_t c = 0; c < cols.size(); ++c) {
                 const uint32_t src = cols[c];
                 tt_all[src] = tt[c];

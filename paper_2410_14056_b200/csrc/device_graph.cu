@@ -88,11 +88,26 @@ const std::vector<uint32_t>& slot_edges(saba_cu_graph* g) {
     const auto& off = g->h_off;
     const auto& adj = host_adj(g);
     std::vector<uint32_t> se(2 * g->m);
-    uint32_t e = 0;
-    for (uint32_t u = 0; u < g->n; ++u)
+    // forward slots (u -> v, v > u) are numbered in CSR order: per-vertex
+    // counts, a prefix sum, then independent numbering and reverse lookups
+    const int64_t N = g->n;
+    std::vector<uint32_t> first(size_t(N) + 1, 0);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t u = 0; u < N; ++u) {
+        uint32_t c = 0;
+        for (uint32_t s = off[u]; s < off[u + 1]; ++s) c += adj[s] > uint32_t(u);
+        first[size_t(u) + 1] = c;
+    }
+    for (int64_t u = 0; u < N; ++u) first[size_t(u) + 1] += first[size_t(u)];
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t u = 0; u < N; ++u) {
+        uint32_t e = first[size_t(u)];
         for (uint32_t s = off[u]; s < off[u + 1]; ++s)
-            if (adj[s] > u) se[s] = e++;
-    for (uint32_t u = 0; u < g->n; ++u)
+            if (adj[s] > uint32_t(u)) se[s] = e++;
+    }
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t ui = 0; ui < N; ++ui) {
+        const uint32_t u = uint32_t(ui);
         for (uint32_t s = off[u]; s < off[u + 1]; ++s)
             if (adj[s] < u) {
                 const uint32_t v = adj[s];
@@ -103,6 +118,7 @@ const std::vector<uint32_t>& slot_edges(saba_cu_graph* g) {
                 }
                 se[s] = se[lo];
             }
+    }
     g->h_slot_edge.swap(se);
     return g->h_slot_edge;
 }

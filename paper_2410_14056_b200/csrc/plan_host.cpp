@@ -21,18 +21,62 @@
 
 namespace saba_cu {
 
-bool host_is_connected(const HostCsr& g) {
-    if (g.n == 0) return false;
-    std::vector<char> seen(g.n, 0);
-    std::vector<uint32_t> q{0};
-    seen[0] = 1;
-    for (size_t h = 0; h < q.size(); ++h)
-        for (uint32_t s = g.off[q[h]]; s < g.off[q[h] + 1]; ++s)
-            if (!seen[g.adj[s]]) {
-                seen[g.adj[s]] = 1;
-                q.push_back(g.adj[s]);
+// Level-synchronous parallel BFS from vertex 0: returns the number of
+// reached vertices and the level parity of each (0xff = unreached).
+uint32_t host_bfs_parity(const HostCsr& g, std::vector<uint8_t>& parity) {
+    parity.assign(g.n, 0xff);
+    if (g.n == 0) return 0;
+    std::vector<uint32_t> frontier{0}, next;
+    parity[0] = 0;
+    uint32_t reached = 1;
+    uint8_t level = 0;
+    while (!frontier.empty()) {
+        ++level;
+        next.clear();
+        const int64_t F = int64_t(frontier.size());
+#pragma omp parallel
+        {
+            std::vector<uint32_t> local;
+#pragma omp for schedule(dynamic, 64) nowait
+            for (int64_t i = 0; i < F; ++i) {
+                const uint32_t u = frontier[size_t(i)];
+                for (uint32_t s = g.off[u]; s < g.off[u + 1]; ++s) {
+                    const uint32_t v = g.adj[s];
+                    if (__atomic_load_n(&parity[v], __ATOMIC_RELAXED) != 0xff) continue;
+                    uint8_t expect = 0xff;
+                    if (__atomic_compare_exchange_n(&parity[v], &expect, uint8_t(level & 1), false,
+                                                    __ATOMIC_RELAXED, __ATOMIC_RELAXED))
+                        local.push_back(v);
+                }
             }
-    return q.size() == g.n;
+#pragma omp critical(saba_bfs_merge)
+            next.insert(next.end(), local.begin(), local.end());
+        }
+        reached += uint32_t(next.size());
+        frontier.swap(next);
+    }
+    return reached;
+}
+
+bool host_is_connected(const HostCsr& g) {
+    std::vector<uint8_t> parity;
+    return g.n > 0 && host_bfs_parity(g, parity) == g.n;
+}
+
+// Connected graphs only: the reference's BFS 2-colouring (graph.hpp:271-292)
+// has its root on side 0, so side = BFS level parity whenever the graph is
+// bipartite, which holds iff no edge joins two vertices of equal parity.
+bool bipartition_connected(const HostCsr& g, const std::vector<uint8_t>& parity,
+                           std::vector<char>& side) {
+    bool bip = true;
+    const int64_t N = g.n;
+#pragma omp parallel for schedule(dynamic, 1024) reduction(&& : bip)
+    for (int64_t u = 0; u < N; ++u)
+        for (uint32_t s = g.off[u]; s < g.off[u + 1]; ++s)
+            if (parity[size_t(u)] == parity[g.adj[s]]) bip = false;
+    side.clear();
+    if (bip) side.assign(parity.begin(), parity.end());
+    return bip;
 }
 
 bool host_bipartition(const HostCsr& g, std::vector<char>& side) {
@@ -134,9 +178,11 @@ Plan host_truncated_lengths(const HostCsr& g, const std::vector<uint32_t>& slot_
     check_arg(eps > 0.0 && eps < 1.0, "truncated_lengths: epsilon must be in (0,1)");
     check_arg(omega >= 1, "truncated_lengths: omega must be >= 1");
     check_arg(max_truncation >= 1, "truncated_lengths: tau_max must be >= 1");
-    check_data(host_is_connected(g), "truncated_lengths: graph must be connected");
+    std::vector<uint8_t> parity;
+    check_data(g.n > 0 && host_bfs_parity(g, parity) == g.n,
+               "truncated_lengths: graph must be connected");
     std::vector<char> side;
-    const bool bip = host_bipartition(g, side);
+    const bool bip = bipartition_connected(g, parity, side);
     Plan p;
     p.bipartite = bip;
     p.lambda_hat = host_estimate_decay(g, omega, bip, side);

@@ -22,6 +22,7 @@ struct Plan {
 };
 
 bool host_is_connected(const HostCsr& g);
+uint32_t host_bfs_parity(const HostCsr& g, std::vector<uint8_t>& parity);
 bool host_bipartition(const HostCsr& g, std::vector<char>& side);
 double host_estimate_decay(const HostCsr& g, uint32_t iters, bool bip, const std::vector<char>& side);
 Plan host_truncated_lengths(const HostCsr& g, const std::vector<uint32_t>& slot_edge, double eps,
