@@ -5,7 +5,7 @@
  *
  * The reference is a header-only C++ library with no plugin or FFI layer
  * (SURVEY §8b): its callers use the C++ API directly. This ABI is what that
- * API lands on; include/saba/*.hpp is the drop-in C++ surface built on it and
+ * API lands on; the headers under include/saba are the drop-in C++ surface built on it and
  * every entry point below names the reference interface it replaces
  * (paths relative to /root/reference/proj/include/saba).
  *

@@ -185,3 +185,12 @@ def write_centrality_tsv(out, g: Graph, values) -> None:
     order = np.lexsort((e[:, 1], e[:, 0]))
     for i in order:
         out.write(f"{int(e[i, 0])}\t{int(e[i, 1])}\t{values[i]:.6g}\n")
+
+
+def aesc_shard_sources(sources, shard_index: int, shard_count: int) -> np.ndarray:
+    """Sources of one shard: every shard_count-th entry starting at
+    shard_index, the interleaved split aesc.cu uses (per-source cost varies
+    ~85x and correlates with vertex id, SURVEY §7 hard part 5)."""
+    if not 0 <= shard_index < shard_count:
+        raise ValueError("bad shard index/count")
+    return np.ascontiguousarray(np.asarray(sources, np.uint32)[shard_index::shard_count])

@@ -251,3 +251,12 @@ def uniform_start_counts(n: int, total_walks: int, master_seed: int = 42) -> np.
         v = scaled_index((counter_hash(s, w) >> np.uint64(32)).astype(np.uint32), n)
         out += np.bincount(v, minlength=n).astype(np.uint64)
     return out
+
+
+def campaign_shard_range(total_walks: int, shard_index: int, shard_count: int):
+    """Walk-list range [r0, r1) of one shard: the partition campaign.cu uses
+    (contiguous ranges of the flattened (vertex, k) list)."""
+    if not 0 <= shard_index < shard_count:
+        raise ValueError("bad shard index/count")
+    return (total_walks * shard_index // shard_count,
+            total_walks * (shard_index + 1) // shard_count)
