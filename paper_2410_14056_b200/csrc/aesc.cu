@@ -44,6 +44,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <exception>
+#include <memory>
+#include <thread>
 #include <cmath>
 #include <vector>
 
@@ -55,6 +58,7 @@
 namespace saba_cu {
 
 constexpr int kCols = 64;           // sources per propagation batch
+constexpr int kDepthsPerGraph = 4;  // propagation depths per CUDA-graph replay
 
 struct AescState {
     uint32_t n_cap = 0;
@@ -74,15 +78,17 @@ struct AescState {
     }
 };
 
+constexpr int kWorkspaces = 2;  // batches in flight (one host thread + stream each)
+
 void release_aesc_state(saba_cu_graph* g) {
-    delete g->aesc;
+    delete[] g->aesc;
     g->aesc = nullptr;
 }
 
 namespace {
 
 // Control block (device): active mask, frozen-at-this-depth mask, dense flag.
-enum { kActive = 0, kFrozenNow = 1, kDense = 2, kDenseReq = 3, kCtrlWords = 4 };
+enum { kActive = 0, kFrozenNow = 1, kDense = 2, kDenseReq = 3, kDepth = 4, kCtrlWords = 8 };
 
 struct AescParams {
     double eps, delta, log_term;  // log_term = log(4m/delta) (aesc.hpp:109)
@@ -161,11 +167,14 @@ __global__ void aesc_init(const uint32_t* __restrict__ col_src, int ncols,
         ctrl[kFrozenNow] = 0;
         ctrl[kDense] = 0;
         ctrl[kDenseReq] = 0;
+        ctrl[kDepth] = 0;
     }
 }
 
 // One thread per column.
-__global__ void aesc_check(uint32_t l, const uint32_t* __restrict__ col_src,
+// The depth l lives in ctrl[kDepth] (so one captured graph serves every
+// depth); the check advances it and resets the next frontier count.
+__global__ void aesc_check(uint32_t* __restrict__ ucount_next, const uint32_t* __restrict__ col_src,
                            const uint32_t* __restrict__ col_tau, const uint2* __restrict__ csr,
                            const uint32_t* __restrict__ tau_slot, AescParams p,
                            const unsigned long long* __restrict__ degsum_cur,
@@ -173,6 +182,7 @@ __global__ void aesc_check(uint32_t l, const uint32_t* __restrict__ col_src,
                            unsigned long long* __restrict__ ctrl) {
     __shared__ unsigned long long frozen;
     const int c = threadIdx.x;
+    const uint32_t l = uint32_t(ctrl[kDepth]);
     if (c == 0) frozen = 0;
     __syncthreads();
     const unsigned long long active = ctrl[kActive];
@@ -193,6 +203,8 @@ __global__ void aesc_check(uint32_t l, const uint32_t* __restrict__ col_src,
         // dense mode switches only between depths, so every kernel of one
         // depth sees the same mode
         if (ctrl[kDenseReq]) ctrl[kDense] = 1;
+        ctrl[kDepth] = l + 1;
+        *ucount_next = 0;
     }
 }
 
@@ -311,6 +323,18 @@ __device__ __forceinline__ void pull_store(uint32_t x, uint32_t deg, double a0, 
     if (mask & hi_mask) ds1 += deg;
 }
 
+// Support degree sums: warp lanes -> shared memory -> one global atomic per
+// column per block (same-address global atomics from every warp serialise in
+// L2 and dominated the pull kernel).
+__device__ __forceinline__ void flush_degsum(unsigned long long* sm, unsigned long long ds0,
+                                             unsigned long long ds1, uint32_t lane,
+                                             unsigned long long* __restrict__ degsum_next) {
+    if (ds0) atomicAdd(sm + 2 * lane, ds0);
+    if (ds1) atomicAdd(sm + 2 * lane + 1, ds1);
+    __syncthreads();
+    if (threadIdx.x < kCols && sm[threadIdx.x]) atomicAdd(degsum_next + threadIdx.x, sm[threadIdx.x]);
+}
+
 // Pull SpMM over the candidate rows (sparse) or all rows (dense) with at
 // most kHeavy neighbours. Warp per row, lane = columns {2 lane, 2 lane + 1}.
 __global__ void __launch_bounds__(256)
@@ -320,8 +344,11 @@ __global__ void __launch_bounds__(256)
               const uint32_t* __restrict__ ulist_next, const uint32_t* __restrict__ ucount_next,
               uint32_t* __restrict__ flag, unsigned long long* __restrict__ degsum_next,
               unsigned long long* __restrict__ ctrl, uint32_t n) {
+    __shared__ unsigned long long bds[kCols];
     const unsigned long long active = ctrl[kActive];
     if (!active) return;
+    if (threadIdx.x < kCols) bds[threadIdx.x] = 0;
+    __syncthreads();
     const bool dense = ctrl[kDense] != 0;
     const uint32_t rows = dense ? n : *ucount_next;
     const uint32_t lane = threadIdx.x & 31;
@@ -337,8 +364,7 @@ __global__ void __launch_bounds__(256)
         pull_store(x, r.y, a0, a1, mask, active, lane, Pn, Qn, Mn, ds0, ds1);
         if (lane == 0 && !dense) flag[x] = 0;
     }
-    if (ds0) atomicAdd(degsum_next + 2 * lane, ds0);  // integer: order-free
-    if (ds1) atomicAdd(degsum_next + 2 * lane + 1, ds1);
+    flush_degsum(bds, ds0, ds1, lane, degsum_next);  // integer sums: order-free
     // switch to dense rows once the frontier covers a quarter of the graph
     if (!dense && blockIdx.x == 0 && threadIdx.x == 0 && rows > n / 4) ctrl[kDenseReq] = 1;
 }
@@ -378,8 +404,11 @@ __global__ void aesc_pull_combine(const uint32_t* __restrict__ heavy_rows,
                                   unsigned long long* __restrict__ Mn, uint32_t* __restrict__ flag,
                                   unsigned long long* __restrict__ degsum_next,
                                   const unsigned long long* __restrict__ ctrl) {
+    __shared__ unsigned long long bds[kCols];
     const unsigned long long active = ctrl[kActive];
     if (!active) return;
+    if (threadIdx.x < kCols) bds[threadIdx.x] = 0;
+    __syncthreads();
     const bool dense = ctrl[kDense] != 0;
     const uint32_t lane = threadIdx.x & 31;
     unsigned long long ds0 = 0, ds1 = 0;
@@ -400,17 +429,17 @@ __global__ void aesc_pull_combine(const uint32_t* __restrict__ heavy_rows,
         __syncwarp();
         if (lane == 0 && !dense) flag[x] = 0;
     }
-    if (ds0) atomicAdd(degsum_next + 2 * lane, ds0);
-    if (ds1) atomicAdd(degsum_next + 2 * lane + 1, ds1);
+    flush_degsum(bds, ds0, ds1, lane, degsum_next);
 }
 
 // Hook (aesc.hpp:581-588) at depth l+1 for the columns that just stepped.
-__global__ void aesc_hook(uint32_t depth, const uint32_t* __restrict__ col_src,
+__global__ void aesc_hook(const uint32_t* __restrict__ col_src,
                           const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
                           const uint32_t* __restrict__ tau_slot, const double* __restrict__ Pn,
                           const unsigned long long* __restrict__ ctrl, double* __restrict__ g_hat) {
     const int c = blockIdx.x;
     if (!((ctrl[kActive] >> c) & 1ull)) return;
+    const uint32_t depth = uint32_t(ctrl[kDepth]);  // l + 1 (advanced by aesc_check)
     const uint32_t src = col_src[c];
     const uint2 r = csr[src];
     const double pi = Pn[size_t(src) * kCols + c] * (1.0 / double(r.y));
@@ -628,10 +657,15 @@ struct Engine {
     std::vector<uint32_t> tau_slot;  // host copy, per directed slot
     uint32_t launches = 0;
     uint64_t pairs = 0, steps = 0;
+    cudaGraphExec_t depth_graph = nullptr;  // kDepthsPerGraph captured depths
 
-    explicit Engine(saba_cu_graph* g_) : g(g_) {
-        if (!g->aesc) g->aesc = new AescState;
-        st = g->aesc;
+    ~Engine() {
+        if (depth_graph) cudaGraphExecDestroy(depth_graph);
+    }
+
+    explicit Engine(saba_cu_graph* g_, int workspace = 0) : g(g_) {
+        if (!g->aesc) g->aesc = new AescState[kWorkspaces];
+        st = &g->aesc[workspace];
         if (!st->stream) {
             SABA_CUDA_CHECK(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
             SABA_CUDA_CHECK(cudaHostAlloc(&st->h_ctrl, sizeof(uint64_t) * kCtrlWords, cudaHostAllocDefault));
@@ -741,37 +775,55 @@ struct Engine {
                                       UC, tflag, tlist, tcount, DS[0], ttd, ctrl, g_hat_dev);
         ++launches;
         const int grid = g->sm_count * 8;
-        int cur = 0;
-        for (uint32_t l = 0;; ++l) {
-            aesc_check<<<1, kCols, 0, s>>>(l, st->col_src.as<uint32_t>(), st->col_tau.as<uint32_t>(),
-                                           csr, tsl, p, DS[cur], DS[cur ^ 1], ttd, ctrl);
+        auto occ_grid = [&](auto kernel) {
+            int occ = 0;
+            SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, 0));
+            return g->sm_count * std::max(occ, 1);
+        };
+        const int grid_pull = occ_grid(aesc_pull), grid_comb = occ_grid(aesc_pull_combine);
+        // One depth (aesc.hpp:391-397 + hook): every argument except the
+        // buffer parity is fixed, the depth itself lives on the device.
+        auto enqueue_depth = [&](int cur) {
+            aesc_check<<<1, kCols, 0, s>>>(UC + (cur ^ 1), st->col_src.as<uint32_t>(),
+                                           st->col_tau.as<uint32_t>(), csr, tsl, p, DS[cur], DS[cur ^ 1],
+                                           ttd, ctrl);
             aesc_rho<<<grid, 256, 0, s>>>(P[cur], csr, UL[cur], UC + cur, ctrl, n, st->R.as<double>());
-            launches += 2;
-            if (l >= lmax) break;
-            // poll the active mask: every depth early on, then every 4 depths
-            if ((l < 4 || (l & 3) == 0) && read_ctrl(kActive) == 0) break;
-            SABA_CUDA_CHECK(cudaMemsetAsync(UC + (cur ^ 1), 0, sizeof(uint32_t), s));
             aesc_expand<<<grid, 256, 0, s>>>(csr, adj, M[cur], UL[cur], UC + cur, UL[cur ^ 1],
                                              UC + (cur ^ 1), flag, tflag, tlist, tcount, ctrl);
             if (st->npieces) {
                 aesc_pull_pieces<<<grid, 256, 0, s>>>(st->pieces.as<HeavyPiece>(), st->npieces, adj,
                                                       Q[cur], M[cur], flag, st->part.as<double>(),
                                                       st->part_mask.as<unsigned long long>(), ctrl);
-                aesc_pull_combine<<<grid, 256, 0, s>>>(
+                aesc_pull_combine<<<grid_comb, 256, 0, s>>>(
                     st->heavy_rows.as<uint32_t>(), st->piece_off.as<uint32_t>(), st->nheavy, csr,
                     st->part.as<double>(), st->part_mask.as<unsigned long long>(), P[cur ^ 1],
                     Q[cur ^ 1], M[cur ^ 1], flag, DS[cur ^ 1], ctrl);
-                launches += 2;
             }
-            aesc_pull<<<grid, 256, 0, s>>>(csr, adj, Q[cur], M[cur], P[cur ^ 1], Q[cur ^ 1], M[cur ^ 1],
+            aesc_pull<<<grid_pull, 256, 0, s>>>(csr, adj, Q[cur], M[cur], P[cur ^ 1], Q[cur ^ 1], M[cur ^ 1],
                                            UL[cur ^ 1], UC + (cur ^ 1), flag, DS[cur ^ 1], ctrl, n);
-            aesc_hook<<<nc, 128, 0, s>>>(l + 1, st->col_src.as<uint32_t>(), csr, adj, tsl, P[cur ^ 1],
-                                         ctrl, g_hat_dev);
-            launches += 3;
-            cur ^= 1;
+            aesc_hook<<<kCols, 128, 0, s>>>(st->col_src.as<uint32_t>(), csr, adj, tsl, P[cur ^ 1], ctrl,
+                                            g_hat_dev);
+        };
+        const uint32_t per_depth = st->npieces ? 7 : 5;
+        if (!depth_graph) {
+            // kDepthsPerGraph depths (even, so the buffer parity returns to 0)
+            // captured once per estimator call and replayed for every batch
+            cudaGraph_t graph;
+            SABA_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            for (int d = 0; d < kDepthsPerGraph; ++d) enqueue_depth(d & 1);
+            SABA_CUDA_CHECK(cudaStreamEndCapture(s, &graph));
+            SABA_CUDA_CHECK(cudaGraphInstantiate(&depth_graph, graph, 0));
+            SABA_CUDA_CHECK(cudaGraphDestroy(graph));
+        }
+        // columns freeze at the latest when l reaches tau_src <= lmax; extra
+        // depths of the last replay only run early-exiting kernels
+        for (uint32_t l = 0; l <= lmax; l += kDepthsPerGraph) {
+            SABA_CUDA_CHECK(cudaGraphLaunch(depth_graph, s));
+            launches += per_depth * kDepthsPerGraph;
+            if (read_ctrl(kActive) == 0) break;
         }
         SABA_CUDA_CHECK(cudaGetLastError());
-        if (parity) *parity = cur;
+        if (parity) *parity = 0;
         std::vector<uint32_t> tt(nc);
         SABA_CUDA_CHECK(cudaMemcpyAsync(tt.data(), ttd, sizeof(uint32_t) * nc, cudaMemcpyDeviceToHost, s));
         SABA_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -991,82 +1043,123 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
         std::stable_sort(list.begin(), list.end(),
                          [&](uint32_t a, uint32_t b) { return E.deg(a) > E.deg(b); });
         std::vector<uint32_t> tt_all(n, 0);
-        cudaEvent_t e0, e1, e2;
-        SABA_CUDA_CHECK(cudaEventCreate(&e0));
-        SABA_CUDA_CHECK(cudaEventCreate(&e1));
-        SABA_CUDA_CHECK(cudaEventCreate(&e2));
-        float prop_ms = 0.f, walk_ms = 0.f;
+        // Batches alternate between kWorkspaces workers, each with its own
+        // buffers, stream and host thread, so one batch's propagation
+        // overlaps another's walk phase. Sources write disjoint g_hat slots.
+        // A second worker pays off only when propagation is deep enough to
+        // overlap with walks; shallow plans are walk-bound and two walk
+        // phases would only contend for DRAM.
+        const int nworkers = plan.max_tau > 31 ? kWorkspaces : 1;
+        std::vector<std::unique_ptr<Engine>> engines;
+        engines.emplace_back(new Engine(std::move(E)));
+        for (int w = 1; w < nworkers; ++w) {
+            engines.emplace_back(new Engine(g, w));
+            engines.back()->p = engines[0]->p;
+            engines.back()->upload_tau(ts);
+        }
+        SABA_CUDA_CHECK(cudaStreamSynchronize(engines[0]->s));  // g_hat zeroed before any batch
+        std::vector<float> prop_ms(kWorkspaces, 0.f), walk_ms(kWorkspaces, 0.f);
+        std::vector<std::exception_ptr> failure(kWorkspaces);
         const auto t0 = std::chrono::steady_clock::now();
-        TileBuilder tb;
-        for (size_t b0 = 0; b0 < list.size(); b0 += kCols) {
-            const std::vector<uint32_t> cols(list.begin() + b0,
-                                             list.begin() + std::min(list.size(), b0 + kCols));
-            SABA_CUDA_CHECK(cudaEventRecord(e0, E.s));
-            const std::vector<uint32_t> tt = E.propagate(cols, d_g);
-            SABA_CUDA_CHECK(cudaEventRecord(e1, E.s));
-            tb.clear();
-            for (size_t c = 0; c < cols.size(); ++c) {
-                const uint32_t src = cols[c];
-                tt_all[src] = tt[c];
-                const uint32_t lo = g->h_off[src], hi = g->h_off[src + 1], deg_i = hi - lo;
-                bool any = false;  // aesc.hpp:592-594
-                for (uint32_t sl = lo; sl < hi && !any; ++sl) any = ts[sl] > tt[c];
-                if (!any) continue;
-                const uint64_t src_seed = substream(substream(cfg->master_seed, kAescTag), src);
-                for (uint32_t sl = lo; sl < hi; ++sl) {
-                    const int64_t tau_eff = int64_t(ts[sl]) - int64_t(tt[c]);
-                    if (tau_eff <= 0) continue;
-                    const uint64_t n_req = walk_budget(uint32_t(tau_eff), cfg->epsilon, cfg->delta, deg_i, m);
-                    check_arg(cfg->switch_depth_cap < 0 || n_req * uint64_t(tau_eff) <= (uint64_t(1) << 26),
-                              "aesc: walk budget infeasible (switch_depth_cap too aggressive for epsilon)");
-                    tb.add(sl, src, hadj[sl], uint32_t(tau_eff + 1), n_req, substream(src_seed, sl),
-                           uint32_t(c));
-                    E.pairs += n_req;
-                    E.steps += 2 * n_req * uint64_t(tau_eff);
+        auto worker = [&](int w) {
+            try {
+                SABA_CUDA_CHECK(cudaSetDevice(g->device));
+                Engine& W = *engines[w];
+                cudaEvent_t e0, e1, e2;
+                SABA_CUDA_CHECK(cudaEventCreate(&e0));
+                SABA_CUDA_CHECK(cudaEventCreate(&e1));
+                SABA_CUDA_CHECK(cudaEventCreate(&e2));
+                TileBuilder tb;
+                for (size_t b0 = size_t(w) * kCols; b0 < list.size(); b0 += size_t(nworkers) * kCols) {
+                    const std::vector<uint32_t> cols(list.begin() + b0,
+                                                     list.begin() + std::min(list.size(), b0 + kCols));
+                    SABA_CUDA_CHECK(cudaEventRecord(e0, W.s));
+                    const std::vector<uint32_t> tt = W.propagate(cols, d_g);
+                    SABA_CUDA_CHECK(cudaEventRecord(e1, W.s));
+                    tb.clear();
+                    for (size_t c = 0; c < cols.size(); ++c) {
+                        const uint32_t src = cols[c];
+                        tt_all[src] = tt[c];
+                        const uint32_t lo = g->h_off[src], hi = g->h_off[src + 1], deg_i = hi - lo;
+                        bool any = false;  // aesc.hpp:592-594
+                        for (uint32_t sl = lo; sl < hi && !any; ++sl) any = ts[sl] > tt[c];
+                        if (!any) continue;
+                        const uint64_t src_seed = substream(substream(cfg->master_seed, kAescTag), src);
+                        for (uint32_t sl = lo; sl < hi; ++sl) {
+                            const int64_t tau_eff = int64_t(ts[sl]) - int64_t(tt[c]);
+                            if (tau_eff <= 0) continue;
+                            const uint64_t n_req =
+                                walk_budget(uint32_t(tau_eff), cfg->epsilon, cfg->delta, deg_i, m);
+                            check_arg(cfg->switch_depth_cap < 0 ||
+                                          n_req * uint64_t(tau_eff) <= (uint64_t(1) << 26),
+                                      "aesc: walk budget infeasible (switch_depth_cap too aggressive for epsilon)");
+                            tb.add(sl, src, hadj[sl], uint32_t(tau_eff + 1), n_req, substream(src_seed, sl),
+                                   uint32_t(c));
+                            W.pairs += n_req;
+                            W.steps += 2 * n_req * uint64_t(tau_eff);
+                        }
+                    }
+                    run_tiles(g, W.st, W.s, tb, W.st->R.as<double>(), cfg->hash_multiplier, d_g, &W.launches);
+                    SABA_CUDA_CHECK(cudaEventRecord(e2, W.s));
+                    W.clear_batch(int(cols.size()));
+                    SABA_CUDA_CHECK(cudaEventSynchronize(e2));
+                    float ta = 0.f, tw = 0.f;
+                    SABA_CUDA_CHECK(cudaEventElapsedTime(&ta, e0, e1));
+                    SABA_CUDA_CHECK(cudaEventElapsedTime(&tw, e1, e2));
+                    prop_ms[w] += ta;
+                    walk_ms[w] += tw;
                 }
+                SABA_CUDA_CHECK(cudaStreamSynchronize(W.s));
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
+                cudaEventDestroy(e2);
+            } catch (...) {
+                failure[w] = std::current_exception();
             }
-            run_tiles(g, E.st, E.s, tb, E.st->R.as<double>(), cfg->hash_multiplier, d_g, &E.launches);
-            SABA_CUDA_CHECK(cudaEventRecord(e2, E.s));
-            E.clear_batch(int(cols.size()));
-            SABA_CUDA_CHECK(cudaEventSynchronize(e2));
-            float a = 0.f, b = 0.f;
-            SABA_CUDA_CHECK(cudaEventElapsedTime(&a, e0, e1));
-            SABA_CUDA_CHECK(cudaEventElapsedTime(&b, e1, e2));
-            prop_ms += a;
-            walk_ms += b;
+        };
+        std::vector<std::thread> threads;
+        for (int w = 1; w < nworkers; ++w) threads.emplace_back(worker, w);
+        worker(0);
+        for (auto& t : threads) t.join();
+        for (auto& f : failure)
+            if (f) std::rethrow_exception(f);
+        Engine& E0 = *engines[0];
+        for (int w = 1; w < nworkers; ++w) {
+            E0.pairs += engines[w]->pairs;
+            E0.steps += engines[w]->steps;
+            E0.launches += engines[w]->launches;
+            prop_ms[0] += prop_ms[w];
+            walk_ms[0] += walk_ms[w];
         }
         const bool full = sources == nullptr && shard_count == 1;
         if (full && s_hat_out) {
-            double* d_s = static_cast<double*>(E.st->s_hat.ensure(sizeof(double) * m));
-            uint32_t* d_se = static_cast<uint32_t*>(E.st->slot_edge_d.ensure(sizeof(uint32_t) * 2 * m));
-            SABA_CUDA_CHECK(cudaMemcpyAsync(d_se, se.data(), sizeof(uint32_t) * 2 * m, cudaMemcpyHostToDevice, E.s));
-            aesc_symmetrise<<<g->sm_count * 4, 256, 0, E.s>>>(g->d_csr, g->d_adj, d_se, n, d_g, d_s);
+            double* d_s = static_cast<double*>(E0.st->s_hat.ensure(sizeof(double) * m));
+            uint32_t* d_se = static_cast<uint32_t*>(E0.st->slot_edge_d.ensure(sizeof(uint32_t) * 2 * m));
+            SABA_CUDA_CHECK(cudaMemcpyAsync(d_se, se.data(), sizeof(uint32_t) * 2 * m, cudaMemcpyHostToDevice, E0.s));
+            aesc_symmetrise<<<g->sm_count * 4, 256, 0, E0.s>>>(g->d_csr, g->d_adj, d_se, n, d_g, d_s);
             SABA_CUDA_CHECK(cudaGetLastError());
-            ++E.launches;
-            SABA_CUDA_CHECK(cudaMemcpyAsync(s_hat_out, d_s, sizeof(double) * m, cudaMemcpyDeviceToHost, E.s));
+            ++E0.launches;
+            SABA_CUDA_CHECK(cudaMemcpyAsync(s_hat_out, d_s, sizeof(double) * m, cudaMemcpyDeviceToHost, E0.s));
         }
-        SABA_CUDA_CHECK(cudaMemcpyAsync(g_hat_out, d_g, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost, E.s));
-        SABA_CUDA_CHECK(cudaStreamSynchronize(E.s));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(g_hat_out, d_g, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost, E0.s));
+        SABA_CUDA_CHECK(cudaStreamSynchronize(E0.s));
         const auto t1 = std::chrono::steady_clock::now();
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        cudaEventDestroy(e2);
         std::copy(plan.tau.begin(), plan.tau.end(), tau_out);
         std::copy(tt_all.begin(), tt_all.end(), tau_tilde_out);
         if (rep) {
             saba_cu_aesc_report r{};
             r.seconds = std::chrono::duration<double>(t1 - t0).count();
             r.plan_seconds = std::chrono::duration<double>(t_plan1 - t_plan0).count();
-            r.propagation_ms = prop_ms;
-            r.walk_ms = walk_ms;
-            r.total_walk_pairs = E.pairs;
-            r.total_walk_steps = E.steps;
+            r.propagation_ms = prop_ms[0];
+            r.walk_ms = walk_ms[0];
+            r.total_walk_pairs = E0.pairs;
+            r.total_walk_steps = E0.steps;
             r.sources = list.size();
             r.lambda_hat = plan.lambda_hat;
             r.bipartite = plan.bipartite;
             r.clamped = plan.clamped;
             r.max_tau = plan.max_tau;
-            r.launches = E.launches;
+            r.launches = E0.launches;
             *rep = r;
         }
     });
