@@ -127,9 +127,9 @@ const std::vector<uint32_t>& slot_edges(saba_cu_graph* g) {
 
 saba_cu_graph::~saba_cu_graph() {
     saba_cu::release_aesc_state(this);
-    if (d_csr) cudaFree(d_csr);
-    if (d_adj) cudaFree(d_adj);
-    if (d_adj_packed) cudaFree(d_adj_packed);
+    if (d_csr) saba_cu::pool_free(d_csr);
+    if (d_adj) saba_cu::pool_free(d_adj);
+    if (d_adj_packed) saba_cu::pool_free(d_adj_packed);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev2) cudaEventDestroy(ev2);
@@ -168,8 +168,14 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
         }
         check_arg(device >= 0 && device < ndev, "device index out of range");
         DeviceScope scope(device);
-        cudaDeviceProp prop;
-        SABA_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+        static cudaDeviceProp props[64];  // queried once per device (slow call)
+        static bool have_props[64] = {};
+        check_arg(device < 64, "device index out of range");
+        if (!have_props[device]) {
+            SABA_CUDA_CHECK(cudaGetDeviceProperties(&props[device], device));
+            have_props[device] = true;
+        }
+        const cudaDeviceProp& prop = props[device];
         check_data(prop.major >= 10, "libsaba_cuda is built for sm_100a (B200)");
 
         auto g = std::make_unique<saba_cu_graph>();
@@ -192,8 +198,8 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
         DevBuf d_offb, d_bad;
         uint32_t* d_off = static_cast<uint32_t*>(d_offb.ensure(sizeof(uint32_t) * (size_t(n) + 1)));
         unsigned int* bad = static_cast<unsigned int*>(d_bad.ensure(sizeof(unsigned int)));
-        SABA_CUDA_CHECK(cudaMalloc(&g->d_csr, sizeof(uint2) * size_t(n)));
-        SABA_CUDA_CHECK(cudaMalloc(&g->d_adj, sizeof(uint32_t) * (two_m ? two_m : 1)));
+        g->d_csr = static_cast<uint2*>(pool_alloc(sizeof(uint2) * size_t(n)));
+        g->d_adj = static_cast<uint32_t*>(pool_alloc(sizeof(uint32_t) * (two_m ? two_m : 1)));
         SABA_CUDA_CHECK(cudaMemcpy(d_off, offsets, sizeof(uint32_t) * (size_t(n) + 1),
                                    cudaMemcpyHostToDevice));
         if (two_m)
@@ -209,7 +215,7 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
         check_data(h_bad == 0, "adjacency id out of range");
         if (n <= kPackMax && two_m) {
             const uint64_t words = (two_m + 2) / 3;
-            SABA_CUDA_CHECK(cudaMalloc(&g->d_adj_packed, sizeof(uint64_t) * words));
+            g->d_adj_packed = static_cast<uint64_t*>(pool_alloc(sizeof(uint64_t) * words));
             pack_adj_kernel<<<g->sm_count * 8, 256>>>(g->d_adj, two_m, g->d_adj_packed);
             SABA_CUDA_CHECK(cudaGetLastError());
         }
