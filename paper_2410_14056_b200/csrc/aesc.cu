@@ -44,6 +44,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <exception>
 #include <memory>
 #include <thread>
@@ -63,6 +64,7 @@ constexpr int kDepthsPerGraph = 4;  // propagation depths per CUDA-graph replay
 struct AescState {
     uint32_t n_cap = 0;
     DevBuf P[2], Q[2], M[2], R;          // n x 64 doubles / uint64 masks / 64 x n rho
+    DevBuf bits;                         // 64 x ceil(n/32) support bitmaps of R (sparse batches)
     DevBuf ulist[2], ucount, flag, tflag, tlist, tcount;
     DevBuf col_src, col_tau, degsum[2], tt, ctrl;  // per-column state
     DevBuf tau_slot, slot_edge_d, g_hat, s_hat, rho1;
@@ -213,7 +215,7 @@ __global__ void aesc_check(uint32_t* __restrict__ ucount_next, const uint32_t* _
 __global__ void aesc_rho(const double* __restrict__ P, const uint2* __restrict__ csr,
                          const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
                          const unsigned long long* __restrict__ ctrl, uint32_t n,
-                         double* __restrict__ R) {
+                         double* __restrict__ R, uint32_t* __restrict__ bits, uint32_t words) {
     const unsigned long long fz = ctrl[kFrozenNow];
     if (!fz) return;
     const bool dense = ctrl[kDense] != 0;
@@ -225,7 +227,9 @@ __global__ void aesc_rho(const double* __restrict__ P, const uint2* __restrict__
         while (f) {
             const int c = __ffsll(f) - 1;
             f &= f - 1;
-            R[size_t(c) * n + v] = P[size_t(v) * kCols + c] * inv;  // p * inv_deg (aesc.hpp:599)
+            const double r = P[size_t(v) * kCols + c] * inv;  // p * inv_deg (aesc.hpp:599)
+            R[size_t(c) * n + v] = r;
+            if (r != 0.0) atomicOr(bits + size_t(c) * words + (v >> 5), 1u << (v & 31));
         }
     }
 }
@@ -454,7 +458,7 @@ __global__ void aesc_hook(const uint32_t* __restrict__ col_src,
 __global__ void aesc_clear(const uint32_t* __restrict__ tlist, const uint32_t* __restrict__ tcount,
                            double* P0, double* P1, double* Q0, double* Q1,
                            unsigned long long* M0, unsigned long long* M1, double* R, uint32_t n,
-                           uint32_t* tflag, int ncols) {
+                           uint32_t* tflag, int ncols, uint32_t* bits, uint32_t words) {
     const uint32_t rows = *tcount;
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < rows;
@@ -465,7 +469,10 @@ __global__ void aesc_clear(const uint32_t* __restrict__ tlist, const uint32_t* _
         reinterpret_cast<double2*>(P1 + size_t(x) * kCols)[lane] = z;
         reinterpret_cast<double2*>(Q0 + size_t(x) * kCols)[lane] = z;
         reinterpret_cast<double2*>(Q1 + size_t(x) * kCols)[lane] = z;
-        for (int c = lane; c < ncols; c += 32) R[size_t(c) * n + x] = 0.0;
+        for (int c = lane; c < ncols; c += 32) {
+            R[size_t(c) * n + x] = 0.0;
+            bits[size_t(c) * words + (x >> 5)] = 0;  // the whole word is cleared anyway
+        }
         if (lane == 0) {
             M0[x] = 0;
             M1[x] = 0;
@@ -528,19 +535,24 @@ __global__ void aesc_keygen(const WalkGroup* __restrict__ groups, const uint32_t
 
 // K4: warps walk consecutive sorted entries (WPT per lane); the score of
 // walk w = sum of rho over steps 1..len-1 in step order (aesc.hpp:491-493).
-template <bool PACKED, int WPT>
+// BITMAP: rho is non-zero only on the landing support; a 1-bit-per-vertex
+// check (64x smaller than rho, L2-resident) skips gathers of exact zeros
+// (adding +0.0 is the identity, so scores are unchanged).
+template <bool PACKED, int WPT, bool BITMAP>
 __global__ void __launch_bounds__(256)
     aesc_walk_sorted(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                      uint32_t nwalks, const WalkGroup* __restrict__ groups,
                      const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
                      const uint64_t* __restrict__ adjp, const double* __restrict__ R, uint32_t n,
-                     uint64_t mult, double* __restrict__ score) {
+                     const uint32_t* __restrict__ bits, uint32_t words, uint64_t mult,
+                     double* __restrict__ score) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     for (uint64_t base = uint64_t(warp) * 32 * WPT; base < nwalks; base += uint64_t(nwarps) * 32 * WPT) {
         uint32_t cur[WPT], seed[WPT], len[WPT], w[WPT];
         const double* rho[WPT];
+        const uint32_t* bm[WPT];
         double sc[WPT];
         uint32_t maxlen = 1;
 #pragma unroll
@@ -552,6 +564,7 @@ __global__ void __launch_bounds__(256)
             cur[r] = 0;
             seed[r] = 0;
             rho[r] = R;
+            bm[r] = bits;
             if (e < nwalks) {
                 w[r] = vals[e];
                 const WalkGroup G = groups[keys[e] >> kSeedBits];
@@ -561,6 +574,7 @@ __global__ void __launch_bounds__(256)
                 cur[r] = side ? G.vj : G.vi;
                 len[r] = G.len;
                 rho[r] = R + size_t(G.col) * n;
+                bm[r] = bits + size_t(G.col) * words;
             }
             maxlen = max(maxlen, len[r]);
         }
@@ -578,7 +592,13 @@ __global__ void __launch_bounds__(256)
                 }
 #pragma unroll
             for (int r = 0; r < WPT; ++r)
-                if (l < len[r]) sc[r] += __ldg(rho[r] + cur[r]);
+                if (l < len[r]) {
+                    if constexpr (BITMAP) {
+                        if ((__ldg(bm[r] + (cur[r] >> 5)) >> (cur[r] & 31)) & 1u) sc[r] += __ldg(rho[r] + cur[r]);
+                    } else {
+                        sc[r] += __ldg(rho[r] + cur[r]);
+                    }
+                }
         }
 #pragma unroll
         for (int r = 0; r < WPT; ++r)
@@ -681,6 +701,8 @@ struct Engine {
                 buf<uint32_t>(st->ulist[b], n);
             }
             SABA_CUDA_CHECK(cudaMemsetAsync(buf<double>(st->R, rows), 0, sizeof(double) * rows, s));
+            SABA_CUDA_CHECK(cudaMemsetAsync(buf<uint32_t>(st->bits, size_t(kCols) * words()), 0,
+                                            sizeof(uint32_t) * kCols * words(), s));
             SABA_CUDA_CHECK(cudaMemsetAsync(buf<uint32_t>(st->flag, n), 0, sizeof(uint32_t) * n, s));
             SABA_CUDA_CHECK(cudaMemsetAsync(buf<uint32_t>(st->tflag, n), 0, sizeof(uint32_t) * n, s));
             buf<uint32_t>(st->tlist, n);
@@ -729,6 +751,8 @@ struct Engine {
     }
 
     uint32_t deg(uint32_t v) const { return g->h_off[v + 1] - g->h_off[v]; }
+    uint32_t words() const { return (g->n + 31) / 32; }
+    bool last_dense = false;  // did the last batch switch to dense rows
 
     uint64_t read_ctrl(int word) {
         SABA_CUDA_CHECK(cudaMemcpyAsync(st->h_ctrl + word, st->ctrl.as<uint64_t>() + word,
@@ -787,7 +811,8 @@ struct Engine {
             aesc_check<<<1, kCols, 0, s>>>(UC + (cur ^ 1), st->col_src.as<uint32_t>(),
                                            st->col_tau.as<uint32_t>(), csr, tsl, p, DS[cur], DS[cur ^ 1],
                                            ttd, ctrl);
-            aesc_rho<<<grid, 256, 0, s>>>(P[cur], csr, UL[cur], UC + cur, ctrl, n, st->R.as<double>());
+            aesc_rho<<<grid, 256, 0, s>>>(P[cur], csr, UL[cur], UC + cur, ctrl, n, st->R.as<double>(),
+                                          st->bits.as<uint32_t>(), words());
             aesc_expand<<<grid, 256, 0, s>>>(csr, adj, M[cur], UL[cur], UC + cur, UL[cur ^ 1],
                                              UC + (cur ^ 1), flag, tflag, tlist, tcount, ctrl);
             if (st->npieces) {
@@ -824,6 +849,7 @@ struct Engine {
         }
         SABA_CUDA_CHECK(cudaGetLastError());
         if (parity) *parity = 0;
+        last_dense = read_ctrl(kDense) != 0;
         std::vector<uint32_t> tt(nc);
         SABA_CUDA_CHECK(cudaMemcpyAsync(tt.data(), ttd, sizeof(uint32_t) * nc, cudaMemcpyDeviceToHost, s));
         SABA_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -840,6 +866,7 @@ struct Engine {
                 SABA_CUDA_CHECK(cudaMemsetAsync(st->M[b].p, 0, sizeof(uint64_t) * n, s));
             }
             SABA_CUDA_CHECK(cudaMemsetAsync(st->R.p, 0, sizeof(double) * size_t(n) * nc, s));
+            SABA_CUDA_CHECK(cudaMemsetAsync(st->bits.p, 0, sizeof(uint32_t) * size_t(words()) * nc, s));
             SABA_CUDA_CHECK(cudaMemsetAsync(st->tflag.p, 0, sizeof(uint32_t) * n, s));
             return;
         }
@@ -847,7 +874,7 @@ struct Engine {
             st->tlist.as<uint32_t>(), st->tcount.as<uint32_t>(), st->P[0].as<double>(),
             st->P[1].as<double>(), st->Q[0].as<double>(), st->Q[1].as<double>(),
             st->M[0].as<unsigned long long>(), st->M[1].as<unsigned long long>(), st->R.as<double>(),
-            n, st->tflag.as<uint32_t>(), nc);
+            n, st->tflag.as<uint32_t>(), nc, st->bits.as<uint32_t>(), words());
         SABA_CUDA_CHECK(cudaGetLastError());
         ++launches;
     }
@@ -914,16 +941,14 @@ int bits_for(uint32_t x) {
 // Walk phase: per chunk keygen -> radix sort (group, seed top bits) -> sorted
 // walks -> pair tiles; then the per-slot fold into g_hat.
 void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb, const double* R,
-               uint64_t mult, double* g_hat_dev, uint32_t* launches) {
+               const uint32_t* bits, uint64_t mult, double* g_hat_dev, uint32_t* launches) {
+    const uint32_t words = (g->n + 31) / 32;
     if (tb.empty()) return;
     double* part = static_cast<double*>(st->partials.ensure(sizeof(double) * std::max(tb.ntiles, 1u)));
     const bool packed = g->d_adj_packed != nullptr;
     constexpr int WPT = 4;
     int occ = 0;
-    if (packed)
-        SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk_sorted<true, WPT>, 256, 0));
-    else
-        SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk_sorted<false, WPT>, 256, 0));
+    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk_sorted<false, WPT, true>, 256, 0));
     for (TileBuilder::Chunk& c : tb.chunks) {
         const uint32_t ng = uint32_t(c.groups.size()), nw = c.walks, nt = uint32_t(c.tiles.size());
         c.offs.push_back(nw);
@@ -947,12 +972,16 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(t, tmp, keys, vals, int(nw), 0, end_bit, s));
         const int grid = int(std::min<uint64_t>((nw + 32 * WPT - 1) / (32 * WPT) * 32 / 256 + 1,
                                                 uint64_t(g->sm_count) * std::max(occ, 1)));
-        if (packed)
-            aesc_walk_sorted<true, WPT><<<grid, 256, 0, s>>>(keys.Current(), vals.Current(), nw, dg, g->d_csr,
-                                                             g->d_adj, g->d_adj_packed, R, g->n, mult, score);
-        else
-            aesc_walk_sorted<false, WPT><<<grid, 256, 0, s>>>(keys.Current(), vals.Current(), nw, dg, g->d_csr,
-                                                              g->d_adj, g->d_adj_packed, R, g->n, mult, score);
+#define SABA_WALK(P, B)                                                                           \
+    aesc_walk_sorted<P, WPT, B><<<grid, 256, 0, s>>>(keys.Current(), vals.Current(), nw, dg, g->d_csr, \
+                                                     g->d_adj, g->d_adj_packed, R, g->n, bits, words,  \
+                                                     mult, score)
+        if (packed) {
+            if (bits) SABA_WALK(true, true); else SABA_WALK(true, false);
+        } else {
+            if (bits) SABA_WALK(false, true); else SABA_WALK(false, false);
+        }
+#undef SABA_WALK
         SABA_CUDA_CHECK(cudaGetLastError());
         aesc_pair_reduce<<<int(std::min<uint32_t>(nt, g->sm_count * 8)), 256, 0, s>>>(dt, nt, dg, score, part);
         SABA_CUDA_CHECK(cudaGetLastError());
@@ -1099,7 +1128,18 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
                             W.steps += 2 * n_req * uint64_t(tau_eff);
                         }
                     }
-                    run_tiles(g, W.st, W.s, tb, W.st->R.as<double>(), cfg->hash_multiplier, d_g, &W.launches);
+                    // sparse supports: skip rho gathers of exact zeros via the bitmap
+                    static const int bitmap_mode = [] {  // 0 off, 1 on, 2 auto
+                        const char* e = getenv("SABA_AESC_BITMAP");
+                        return e ? atoi(e) : 2;
+                    }();
+                    // auto: supports of a few propagation steps are small even
+                    // when the batch's union frontier went dense
+                    const uint32_t tt_max = *std::max_element(tt.begin(), tt.end());
+                    const bool use_bits = bitmap_mode == 1 || (bitmap_mode == 2 && tt_max <= 4);
+                    run_tiles(g, W.st, W.s, tb, W.st->R.as<double>(),
+                              use_bits ? W.st->bits.as<uint32_t>() : nullptr, cfg->hash_multiplier,
+                              d_g, &W.launches);
                     SABA_CUDA_CHECK(cudaEventRecord(e2, W.s));
                     W.clear_batch(int(cols.size()));
                     SABA_CUDA_CHECK(cudaEventSynchronize(e2));
@@ -1218,7 +1258,7 @@ int saba_cu_estimate_edge(saba_cu_graph* g, uint32_t v_i, uint32_t v_j, const do
         TileBuilder tb;
         tb.add(0, v_i, v_j, tau_eff + 1, n_req, edge_seed, 0);
         uint32_t launches = 0;
-        run_tiles(g, E.st, E.s, tb, d_rho, mult, d_out, &launches);
+        run_tiles(g, E.st, E.s, tb, d_rho, nullptr, mult, d_out, &launches);
         SABA_CUDA_CHECK(cudaMemcpyAsync(out, d_out, sizeof(double), cudaMemcpyDeviceToHost, E.s));
         SABA_CUDA_CHECK(cudaStreamSynchronize(E.s));
     });
