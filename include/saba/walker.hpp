@@ -183,7 +183,6 @@ struct CampaignReport {
 namespace detail {
 inline CampaignReport campaign_on_gpu(const Graph& g, const CampaignConfig& cfg, uint64_t total_walks,
                                       std::vector<uint64_t>& counts) {
-    check_arg(!cfg.collect_stats, "collect_stats is not supported on GPU");
     saba_cu_campaign_config c{};
     c.walks_per_vertex = cfg.walks_per_vertex;
     c.total_walks = total_walks;
@@ -203,6 +202,17 @@ inline CampaignReport campaign_on_gpu(const Graph& g, const CampaignConfig& cfg,
     rep.seconds = r.seconds;
     rep.total_steps = r.total_steps;
     rep.total_events = r.total_events;
+    if (cfg.collect_stats && cfg.length > 1) {  // the untimed stats pass (walker.hpp:471, 526-536)
+        std::vector<uint64_t> hist(size_t(cfg.lanes) + 1), per_step(cfg.length - 1), tot(4);
+        detail::raise_on(saba_cu_branching_stats(g.device_handle(), &c, hist.data(), per_step.data(),
+                                                 tot.data()),
+                         "branching statistics");
+        rep.has_stats = true;
+        rep.branching = branching_stats(std::span<const uint64_t>(hist));
+        rep.branching.mean_candidate_degree = tot[2] ? double(tot[3]) / double(tot[2]) : 0.0;
+        rep.proxy.per_step = std::move(per_step);
+        rep.proxy.total = tot[0];
+    }
     return rep;
 }
 }  // namespace detail

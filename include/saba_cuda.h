@@ -159,6 +159,17 @@ SABA_API int saba_cu_walk_campaign_device(saba_cu_graph* g, const saba_cu_campai
                                  uint64_t* counts_dev, void* stream, int timing,
                                  saba_cu_campaign_report* report);
 
+/* Branching statistics of the campaign's bouquets (BranchCollector,
+ * walker.hpp:64-109 as driven by campaign_vertex_scaled, 430-449): bouquets
+ * are `lanes` consecutive entries of each start vertex's (Saba: sorted) seed
+ * list; per bouquet step the distinct lane vertices are counted.
+ * histogram_out[lanes+1], per_step_out[length-1] (distinct-access proxy,
+ * bench.hpp:45-50), totals_out[4] = {total_distinct, samples, lane_steps,
+ * degree_sum}. Unsharded; length > 1. */
+SABA_API int saba_cu_branching_stats(saba_cu_graph* g, const saba_cu_campaign_config* cfg,
+                                     uint64_t* histogram_out, uint64_t* per_step_out,
+                                     uint64_t* totals_out);
+
 /* ======================================================================
  * TGT+ AESC (aesc.hpp)
  * ==================================================================== */

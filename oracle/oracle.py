@@ -276,6 +276,8 @@ class Reference:
         L.ref_campaign_kv.argtypes = [C.c_void_p, u64p, C.c_uint64, C.c_uint32, C.c_int,
                                       C.c_uint32, C.c_int, C.c_uint64, C.c_uint64, C.c_uint32,
                                       C.c_uint32, u64p, f64p, u64p]
+        L.ref_campaign_stats.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.c_uint32,
+                                         C.c_int, C.c_uint64, C.c_uint64, u64p, u64p, u64p, f64p, f64p]
         L.ref_max_threads.restype = C.c_int
         L.ref_walk_budget.argtypes = [C.c_uint32, C.c_double, C.c_double, C.c_uint32, C.c_uint64,
                                       u64p]
@@ -337,6 +339,17 @@ class Reference:
         self._chk(self.lib.ref_campaign(g.h, K, L, mode, lanes, threads, master, mult,
                                         _p(out, u64p), C.byref(sec), C.byref(steps)), "campaign")
         return out, sec.value, steps.value
+
+    def campaign_stats(self, g, K, L, mode=3, lanes=8, threads=0, master=42, mult=DEFAULT_MULT):
+        hist = np.zeros(lanes + 1, np.uint64)
+        step = np.zeros(L - 1, np.uint64)
+        out4 = np.zeros(4, np.uint64)
+        md = C.c_double()
+        mean = C.c_double()
+        self._chk(self.lib.ref_campaign_stats(g.h, K, L, mode, lanes, threads, master, mult,
+                                              _p(hist, u64p), _p(step, u64p), _p(out4, u64p),
+                                              C.byref(md), C.byref(mean)), "campaign_stats")
+        return hist, step, int(out4[0]), int(out4[1]), md.value, mean.value
 
     def campaign_kv(self, g, L, W=0, k_per_vertex=None, sorted_=True, lanes=8, threads=0,
                     master=42, mult=DEFAULT_MULT, vertex_stride=1, vertex_phase=0):

@@ -150,6 +150,37 @@ REF_API int ref_campaign(void* h, uint64_t K, uint32_t L, int mode, uint32_t lan
     });
 }
 
+// run_walk_campaign with collect_stats = true (walker.hpp:470-536): the
+// reference's BranchCollector output. hist[lanes+1], per_step[L-1],
+// out4 = {proxy.total, branching.samples, 0, 0}, mean_deg = mean_candidate_degree.
+REF_API int ref_campaign_stats(void* h, uint64_t K, uint32_t L, int mode, uint32_t lanes,
+                               int threads, uint64_t master, uint64_t mult, uint64_t* hist,
+                               uint64_t* per_step, uint64_t* out4, double* mean_deg,
+                               double* mean) {
+    return guarded([&] {
+        const saba::Graph& g = *as_graph(h);
+        saba::CampaignConfig cfg;
+        cfg.walks_per_vertex = K;
+        cfg.length = L;
+        cfg.mode = static_cast<saba::WalkMode>(mode);
+        cfg.lanes = lanes;
+        cfg.threads = threads;
+        cfg.master_seed = master;
+        cfg.collect_stats = true;
+        cfg.hash = saba::HashSpec{mult};
+        saba::VisitCountSink sink(g.vertex_count());
+        const saba::CampaignReport rep = saba::run_walk_campaign(g, cfg, sink);
+        saba::check_data(rep.has_stats, "no stats collected");
+        std::memcpy(hist, rep.branching.histogram.data(), sizeof(uint64_t) * (lanes + 1));
+        std::memcpy(per_step, rep.proxy.per_step.data(), sizeof(uint64_t) * (L - 1));
+        out4[0] = rep.proxy.total;
+        out4[1] = rep.branching.samples;
+        out4[2] = out4[3] = 0;
+        *mean_deg = rep.branching.mean_candidate_degree;
+        *mean = rep.branching.mean;
+    });
+}
+
 // Uniform-random-start campaign: K_v walks of v are the
 // reference's own campaign_vertex_scaled<Sorted>(g, v, K_v, ...) with
 // vseed = substream(master, v), driven by the same OpenMP schedule and

@@ -198,6 +198,100 @@ void launch_walk(const saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_
     }
 }
 
+// Branching statistics (BranchCollector, walker.hpp:64-109, 234, 430-449):
+// block per start vertex. The vertex's K_v seeds are generated and (Saba)
+// sorted in shared memory, so the reference's bouquets — `lanes` consecutive
+// entries of the vertex's sorted seed list — are rebuilt exactly; each thread
+// replays whole bouquets and records, per step, the number of distinct lane
+// vertices and the degree sum at selection time. Integer sums: order-free.
+// smem: K_v seeds (u32, padded to a power of two) | hist[lanes+1] | per_step[L-1]
+__global__ void branch_stats_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                                    const uint64_t* __restrict__ adjp_unused, uint32_t n,
+                                    const uint32_t* __restrict__ kv, uint64_t k_uniform,
+                                    uint32_t kpad, uint32_t L, uint32_t lanes, int sorted,
+                                    uint64_t master, uint64_t mult,
+                                    unsigned long long* __restrict__ hist,
+                                    unsigned long long* __restrict__ per_step,
+                                    unsigned long long* __restrict__ totals) {
+    extern __shared__ unsigned long long smem_u64[];
+    unsigned long long* s_hist = smem_u64;
+    unsigned long long* s_step = s_hist + (lanes + 1);
+    uint32_t* seeds = reinterpret_cast<uint32_t*>(s_step + (L - 1));
+    for (uint32_t i = threadIdx.x; i < lanes + 1 + (L - 1); i += blockDim.x) smem_u64[i] = 0;
+    unsigned long long t_distinct = 0, t_samples = 0, t_lane_steps = 0, t_degsum = 0;
+    for (uint32_t v = blockIdx.x; v < n; v += gridDim.x) {
+        const uint32_t K = kv ? kv[v] : uint32_t(k_uniform);
+        if (K == 0) continue;
+        const uint64_t vseed = substream(master, v);
+        __syncthreads();
+        const uint32_t P = sorted ? kpad : K;
+        for (uint32_t k = threadIdx.x; k < P; k += blockDim.x)
+            seeds[k] = k < K ? walk_seed(vseed, k) : 0xffffffffu;  // padding sorts last
+        __syncthreads();
+        if (sorted) {  // bitonic sort of the padded seed list (walker.hpp:439)
+            for (uint32_t size = 2; size <= P; size <<= 1)
+                for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                        const uint32_t j = i ^ stride;
+                        if (j > i) {
+                            const bool up = (i & size) == 0;
+                            const uint32_t a = seeds[i], b = seeds[j];
+                            if ((a > b) == up) {
+                                seeds[i] = b;
+                                seeds[j] = a;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+        }
+        const uint32_t nb = (K + lanes - 1) / lanes;
+        for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+            const uint32_t act = min(lanes, K - b * lanes);
+            uint32_t cur[64], tmp[64];
+            for (uint32_t i = 0; i < act; ++i) cur[i] = v;
+            for (uint32_t l = 1; l < L; ++l) {
+                unsigned long long degsum = 0;
+                for (uint32_t i = 0; i < act; ++i) {
+                    const uint2 rec = ldg_csr(csr + cur[i]);
+                    degsum += rec.y;
+                    const uint32_t raw = seeds[b * lanes + i] ^ hash_state(mult, cur[i], l);
+                    cur[i] = ldg_u32(adj + rec.x + scaled_index(raw, rec.y));
+                }
+                // distinct lane vertices (insertion sort, walker.hpp:77-90)
+                for (uint32_t i = 0; i < act; ++i) {
+                    const uint32_t x = cur[i];
+                    uint32_t j = i;
+                    while (j > 0 && tmp[j - 1] > x) {
+                        tmp[j] = tmp[j - 1];
+                        --j;
+                    }
+                    tmp[j] = x;
+                }
+                uint32_t distinct = 1;
+                for (uint32_t i = 1; i < act; ++i) distinct += tmp[i] != tmp[i - 1];
+                atomicAdd(s_hist + distinct, 1ull);
+                atomicAdd(s_step + (l - 1), (unsigned long long)distinct);
+                t_distinct += distinct;
+                t_samples += 1;
+                t_lane_steps += act;
+                t_degsum += degsum;
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < lanes + 1; i += blockDim.x)
+        if (s_hist[i]) atomicAdd(hist + i, s_hist[i]);
+    for (uint32_t i = threadIdx.x; i < L - 1; i += blockDim.x)
+        if (s_step[i]) atomicAdd(per_step + i, s_step[i]);
+    if (t_samples) {
+        atomicAdd(totals + 0, t_distinct);
+        atomicAdd(totals + 1, t_samples);
+        atomicAdd(totals + 2, t_lane_steps);
+        atomicAdd(totals + 3, t_degsum);
+    }
+}
+
 // One thread per walk; materialises the path (random_walk, walker.hpp:283-302).
 __global__ void walk_paths_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
                                   const uint32_t* __restrict__ starts,
@@ -381,6 +475,53 @@ int saba_cu_walk_campaign_device(saba_cu_graph* g, const saba_cu_campaign_config
         }
         fill_report(g, *cfg, w, &r);
         if (rep) *rep = r;
+    });
+}
+
+int saba_cu_branching_stats(saba_cu_graph* g, const saba_cu_campaign_config* cfg,
+                            uint64_t* histogram_out, uint64_t* per_step_out, uint64_t* totals_out) {
+    return guard([&] {
+        check_arg(g && cfg && histogram_out && per_step_out && totals_out, "null argument");
+        validate_campaign(g, *cfg);
+        check_arg(cfg->length > 1, "branching statistics need walks of length > 1");
+        check_arg(cfg->shard_count == 1, "branching statistics are computed unsharded");
+        DeviceScope scope(g->device);
+        const uint32_t n = g->n, L = cfg->length, lanes = cfg->lanes;
+        uint32_t* kv = nullptr;
+        uint64_t kmax = cfg->walks_per_vertex;
+        DevBuf d_kv;
+        if (cfg->total_walks > 0) {
+            kv = static_cast<uint32_t*>(d_kv.ensure(sizeof(uint32_t) * n));
+            SABA_CUDA_CHECK(cudaMemset(kv, 0, sizeof(uint32_t) * n));
+            const int hb = int(std::min<uint64_t>((cfg->total_walks + 255) / 256, uint64_t(g->sm_count) * 16));
+            start_hist_kernel<<<hb, 256>>>(cfg->total_walks, substream(cfg->master_seed, kStartTag), n, kv);
+            SABA_CUDA_CHECK(cudaGetLastError());
+            std::vector<uint32_t> h(n);
+            SABA_CUDA_CHECK(cudaMemcpy(h.data(), kv, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+            kmax = *std::max_element(h.begin(), h.end());
+        }
+        uint32_t kpad = 1;
+        while (kpad < kmax) kpad <<= 1;
+        const size_t smem = sizeof(uint64_t) * (lanes + L) + sizeof(uint32_t) * kpad;
+        check_arg(smem <= 220 * 1024, "branching statistics: too many walks per vertex or steps for one block");
+        SABA_CUDA_CHECK(cudaFuncSetAttribute(branch_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(smem)));
+        DevBuf d_hist, d_step, d_tot;
+        auto* hist = static_cast<unsigned long long*>(d_hist.ensure(sizeof(uint64_t) * (lanes + 1)));
+        auto* step = static_cast<unsigned long long*>(d_step.ensure(sizeof(uint64_t) * (L - 1)));
+        auto* tot = static_cast<unsigned long long*>(d_tot.ensure(sizeof(uint64_t) * 4));
+        SABA_CUDA_CHECK(cudaMemset(hist, 0, sizeof(uint64_t) * (lanes + 1)));
+        SABA_CUDA_CHECK(cudaMemset(step, 0, sizeof(uint64_t) * (L - 1)));
+        SABA_CUDA_CHECK(cudaMemset(tot, 0, sizeof(uint64_t) * 4));
+        const int blocks = int(std::min<uint64_t>(n, uint64_t(g->sm_count) * 8));
+        branch_stats_kernel<<<blocks, 256, smem>>>(g->d_csr, g->d_adj, g->d_adj_packed, n, kv,
+                                                   cfg->walks_per_vertex, kpad, L, lanes,
+                                                   cfg->mode == SABA_MODE_SABA, cfg->master_seed,
+                                                   cfg->hash_multiplier, hist, step, tot);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        SABA_CUDA_CHECK(cudaMemcpy(histogram_out, hist, sizeof(uint64_t) * (lanes + 1), cudaMemcpyDeviceToHost));
+        SABA_CUDA_CHECK(cudaMemcpy(per_step_out, step, sizeof(uint64_t) * (L - 1), cudaMemcpyDeviceToHost));
+        SABA_CUDA_CHECK(cudaMemcpy(totals_out, tot, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -180,6 +180,45 @@ class CampaignConfig:
 
 
 @dataclass
+class BranchingStats:
+    """walker.hpp:111-118."""
+    lanes: int = 0
+    histogram: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+    samples: int = 0
+    mean: float = 0.0
+    p1: int = 0
+    p10: int = 0
+    p25: int = 0
+    mean_candidate_degree: float = 0.0
+
+
+@dataclass
+class DistinctProxy:
+    per_step: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+    total: int = 0
+
+
+def branching_stats(histogram) -> BranchingStats:
+    """Percentiles (ceil(q * total)-th, 1-based) and mean of a distinct-lanes
+    histogram (walker.hpp:122-151)."""
+    h = np.asarray(histogram, np.uint64)
+    total = int(h.sum())
+    if total == 0:
+        raise ValueError("branching_stats: empty trace")
+    weighted = 0.0
+    for c, x in enumerate(h):  # same accumulation order as the reference
+        weighted += float(c) * float(x)
+    cum = np.cumsum(h.astype(np.int64))
+
+    def pct(q):
+        rank = max(1, int(np.ceil(q * float(total))))
+        return int(np.searchsorted(cum, rank))
+
+    return BranchingStats(max(len(h) - 1, 0), h.copy(), total, weighted / float(total),
+                          pct(0.01), pct(0.10), pct(0.25))
+
+
+@dataclass
 class CampaignReport:
     seconds: float = 0.0
     total_steps: int = 0
@@ -189,6 +228,8 @@ class CampaignReport:
     walk_kernel_ms: float = 0.0
     launches: int = 0
     shard_walks: int = 0
+    branching: BranchingStats | None = None
+    proxy: DistinctProxy | None = None
 
 
 def _cfg_c(cfg: CampaignConfig, total_walks: int, shard_index: int, shard_count: int):
@@ -214,8 +255,6 @@ def run_walk_campaign(g: Graph, cfg: CampaignConfig, sink: VisitCountSink, *,
     """
     if not isinstance(sink, VisitCountSink):
         raise TypeError("the GPU campaign supports VisitCountSink only")
-    if cfg.collect_stats:
-        raise ValueError("collect_stats is not supported on GPU yet")
     if len(sink.counts) != g.n:
         raise ValueError("sink size != vertex count")
     counts = np.zeros(g.n, np.uint64)
@@ -224,7 +263,29 @@ def run_walk_campaign(g: Graph, cfg: CampaignConfig, sink: VisitCountSink, *,
     L.check(L.lib().saba_cu_walk_campaign(g.device_handle(device), C.byref(c),
                                           L.ptr(counts, L.u64p), C.byref(rep)), "walk_campaign")
     sink.counts += counts
-    return _report(rep)
+    out = _report(rep)
+    # the reference collects stats in lane modes with L > 1 (walker.hpp:471)
+    if cfg.collect_stats and cfg.length > 1:
+        out.branching, out.proxy = collect_branching(g, cfg, total_walks=total_walks,
+                                                     device=device)
+        out.has_stats = True
+    return out
+
+
+def collect_branching(g: Graph, cfg: CampaignConfig, *, total_walks: int = 0, device: int = 0):
+    """Branching statistics of the campaign's bouquets (walker.hpp:64-109,
+    526-536) computed on the GPU (the reference's untimed stats pass,
+    bench.hpp:171-178)."""
+    hist = np.zeros(cfg.lanes + 1, np.uint64)
+    step = np.zeros(cfg.length - 1, np.uint64)
+    tot = np.zeros(4, np.uint64)
+    c = _cfg_c(cfg, total_walks, 0, 1)
+    L.check(L.lib().saba_cu_branching_stats(g.device_handle(device), C.byref(c), L.ptr(hist, L.u64p),
+                                            L.ptr(step, L.u64p), L.ptr(tot, L.u64p)),
+            "branching_stats")
+    st = branching_stats(hist)
+    st.mean_candidate_degree = float(tot[3]) / float(tot[2]) if tot[2] else 0.0
+    return st, DistinctProxy(step, int(tot[0]))
 
 
 def run_walk_campaign_device(g: Graph, cfg: CampaignConfig, counts_dev_ptr: int, stream_ptr: int = 0,

@@ -87,6 +87,17 @@ def main():
     c, _, _ = R.campaign_kv(G["sf2000_8_17"], 16, W=32768, master=42, threads=4)
     out["ucamp/sf2000_8_17/W32768_L16_s42"] = c
 
+    # branching statistics (test_walker.cpp:207-282 shapes)
+    stats = [("P2", 64, 5, 3, 8, 42), ("K9", 4096, 2, 2, 8, 42), ("sf2000_8_17", 2048, 10, 3, 8, 42),
+             ("sf2000_8_17", 2048, 10, 2, 8, 42), ("sf400_5_21", 64, 7, 3, 16, 9),
+             ("sf400_5_21", 13, 7, 3, 8, 9)]
+    for gname, K, L, mode, lanes, seed in stats:
+        hist, step, total, samples, mdeg, mean = R.campaign_stats(G[gname], K, L, mode, lanes,
+                                                                  threads=4, master=seed)
+        key = f"stats/{gname}/K{K}_L{L}_m{mode}_b{lanes}_s{seed}"
+        out[key + "/hist"], out[key + "/per_step"] = hist, step
+        out[key + "/scalars"] = np.array([total, samples, mdeg, mean], np.float64)
+
     # walk budget (test_aesc.cpp:27 and a grid)
     wb = []
     for t in (1, 5, 13, 97):

@@ -176,3 +176,43 @@ def test_device_variant_matches_host_variant(sb):
     sb.run_walk_campaign_device(g, cfg, counts.data_ptr(), st.cuda_stream, total_walks=200000)
     torch.cuda.synchronize()
     assert np.array_equal(counts.cpu().numpy().astype(np.uint64), sink.counts)
+
+
+def test_branching_statistics_match_reference(golden, sb):
+    """BranchCollector output (walker.hpp:64-109) of the reference's campaign
+    with collect_stats, rebuilt on the GPU bouquet for bouquet."""
+    n = 0
+    for key in golden:
+        if not (key.startswith("stats/") and key.endswith("/hist")):
+            continue
+        base = key[: -len("/hist")]
+        _, gname, spec = base.split("/")
+        K, L, mode, lanes, seed = (int(x[1:]) for x in spec.split("_"))
+        g = golden_graph(golden, gname)
+        cfg = sb.CampaignConfig(walks_per_vertex=K, length=L, mode=sb.WalkMode(mode), lanes=lanes,
+                                master_seed=seed, collect_stats=True)
+        rep = sb.run_walk_campaign(g, cfg, sb.VisitCountSink(g.n))
+        total, samples, mdeg, mean = golden[base + "/scalars"]
+        assert rep.has_stats
+        assert np.array_equal(rep.branching.histogram, golden[key]), base
+        assert np.array_equal(rep.proxy.per_step, golden[base + "/per_step"]), base
+        assert rep.proxy.total == int(total) and rep.branching.samples == int(samples)
+        assert rep.branching.mean_candidate_degree == mdeg and rep.branching.mean == mean
+        n += 1
+    assert n >= 6
+    # test_walker.cpp:227-241: forced lanes -> one distinct vertex per step
+    p2 = sb.path(2)
+    rep = sb.run_walk_campaign(p2, sb.CampaignConfig(walks_per_vertex=64, length=5, collect_stats=True),
+                               sb.VisitCountSink(2))
+    assert rep.branching.mean == 1.0 and rep.branching.p1 == 1 and rep.branching.p25 == 1
+
+
+def test_saba_clusters_bouquets(golden, sb):
+    """test_walker.cpp:259-282: sorted seeds give fewer distinct lanes."""
+    g = golden_graph(golden, "sf2000_8_17")
+    run = lambda m: sb.run_walk_campaign(  # noqa: E731
+        g, sb.CampaignConfig(walks_per_vertex=2048, length=10, mode=m, collect_stats=True),
+        sb.VisitCountSink(g.n))
+    h, s = run(sb.WalkMode.Hash), run(sb.WalkMode.Saba)
+    assert s.branching.mean < h.branching.mean
+    assert s.proxy.per_step[0] <= h.proxy.per_step[0]
