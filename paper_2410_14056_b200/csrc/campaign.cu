@@ -121,6 +121,85 @@ __global__ void __launch_bounds__(kWalkThreads)
     }
 }
 
+// Fat adjacency: slot s -> adj[s] | base(adj[s]) << idb | degree(adj[s]) << sh.
+__global__ void build_fat_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                                 uint64_t two_m, uint32_t idb, uint32_t sh, uint64_t* __restrict__ fat) {
+    for (uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < two_m;
+         s += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t v = adj[s];
+        const uint2 r = csr[v];
+        fat[s] = uint64_t(v) | (uint64_t(r.x) << idb) | (uint64_t(r.y) << sh);
+    }
+}
+
+// K2 over the fat adjacency: the {base, degree} of the next vertex arrives
+// with its id, so each step is ONE dependent gather + the visit reduction.
+template <int WPT, bool AGG>
+__global__ void __launch_bounds__(kWalkThreads)
+    walk_count_fat_kernel(const uint2* __restrict__ csr, const uint64_t* __restrict__ fat,
+                          uint32_t idb, uint32_t sh, const uint64_t* __restrict__ keys,
+                          uint64_t nwalks, uint32_t L, uint64_t mult,
+                          unsigned long long* __restrict__ counts) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    const uint64_t idmask = (uint64_t(1) << idb) - 1, bmask = (uint64_t(1) << (sh - idb)) - 1;
+    for (uint64_t base = warp * 32 * WPT; base < nwalks; base += nwarps * 32 * WPT) {
+        uint32_t cur[WPT], seed[WPT], sbase[WPT], deg[WPT];
+        bool act[WPT];
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {
+            const uint64_t i = base + uint64_t(r) * 32 + lane;
+            act[r] = i < nwalks;
+            const uint64_t k = act[r] ? __ldcs(reinterpret_cast<const unsigned long long*>(keys) + i) : 0;
+            cur[r] = uint32_t(k >> 32);
+            seed[r] = uint32_t(k);
+            const uint2 rec = act[r] ? ldg_csr(csr + cur[r]) : make_uint2(0, 1);
+            sbase[r] = rec.x;
+            deg[r] = rec.y;
+        }
+        for (uint32_t l = 1; l < L; ++l) {
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) {
+                const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
+                const uint64_t f = act[r] ? __ldg(reinterpret_cast<const unsigned long long*>(fat) +
+                                                  sbase[r] + scaled_index(raw, deg[r]))
+                                          : 0ull;
+                cur[r] = uint32_t(f & idmask);
+                sbase[r] = uint32_t((f >> idb) & bmask);
+                deg[r] = uint32_t(f >> sh);
+            }
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) {
+                if constexpr (AGG)
+                    warp_count_visit(counts, cur[r], act[r], lane);
+                else
+                    count_visit(counts, cur[r], act[r]);
+            }
+        }
+    }
+}
+
+bool ensure_fat(saba_cu_graph* g) {
+    if (g->fat_tried) return g->d_adj_fat != nullptr;
+    g->fat_tried = true;
+    auto bits = [](uint64_t x) {  // bits to represent values in [0, x]
+        uint32_t b = 1;
+        while (b < 64 && (uint64_t(1) << b) <= x) ++b;
+        return b;
+    };
+    const uint32_t idb = bits(g->n ? g->n - 1 : 0), bb = bits(2 * g->m), db = bits(g->max_degree);
+    if (idb + bb + db > 64 || g->m == 0) return false;
+    g->fat_idb = idb;
+    g->fat_sh = idb + bb;
+    g->d_adj_fat = static_cast<uint64_t*>(pool_alloc(sizeof(uint64_t) * 2 * g->m));
+    build_fat_kernel<<<g->sm_count * 8, 256>>>(g->d_csr, g->d_adj, 2 * g->m, g->fat_idb, g->fat_sh,
+                                               g->d_adj_fat);
+    SABA_CUDA_CHECK(cudaGetLastError());
+    SABA_CUDA_CHECK(cudaDeviceSynchronize());
+    return true;
+}
+
 __global__ void add_counts_kernel(const uint32_t* __restrict__ c32, uint32_t n,
                                   unsigned long long* __restrict__ counts) {
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
@@ -136,6 +215,7 @@ struct WalkVariant {
     bool c32 = false;
     bool agg = true;
     int blocks_per_sm = 0;  // 0 = occupancy maximum
+    int fat = -1;           // one-gather steps over the fat adjacency: 1 on, 0 off, -1 auto
 };
 
 WalkVariant walk_variant() {
@@ -152,6 +232,7 @@ WalkVariant walk_variant() {
             w.c32 = get("c32=", w.c32) != 0;
             w.agg = get("agg=", w.agg) != 0;
             w.blocks_per_sm = get("bps=", 0);
+            w.fat = get("fat=", w.fat);
         }
         return w;
     }();
@@ -186,9 +267,36 @@ void launch_walk_w(const saba_cu_graph* g, const WalkVariant& v, bool packed, bo
 #undef SABA_LW
 }
 
-void launch_walk(const saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, uint32_t L,
+template <int WPT, bool A>
+void launch_fat_t(saba_cu_graph* g, int bps, const uint64_t* keys, uint64_t nw, uint32_t L,
+                  uint64_t mult, void* counts, cudaStream_t st) {
+    auto k = walk_count_fat_kernel<WPT, A>;
+    int occ = 0;
+    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWalkThreads, 0));
+    if (bps <= 0 || bps > occ) bps = occ > 0 ? occ : 1;
+    k<<<g->sm_count * bps, kWalkThreads, 0, st>>>(g->d_csr, g->d_adj_fat, g->fat_idb, g->fat_sh, keys,
+                                                  nw, L, mult, static_cast<unsigned long long*>(counts));
+    SABA_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, uint32_t L,
                  uint64_t mult, void* counts, cudaStream_t st) {
     const WalkVariant v = walk_variant();
+    // auto: the fat array (8 B/slot) pays off while it stays L2-resident;
+    // beyond that the packed 2.67 B/slot adjacency moves fewer DRAM bytes
+    // (cfg1: 24% faster fat, cfg2: 21% slower; profiles/r01_walk_variant_sweep2.txt)
+    const bool want_fat = v.fat == 1 || (v.fat == -1 && 16 * g->m <= (uint64_t(48) << 20));
+    if (want_fat && !c32 && ensure_fat(g)) {
+        switch (v.wpt) {
+            case 2: v.agg ? launch_fat_t<2, true>(g, v.blocks_per_sm, keys, nw, L, mult, counts, st)
+                          : launch_fat_t<2, false>(g, v.blocks_per_sm, keys, nw, L, mult, counts, st); break;
+            case 8: v.agg ? launch_fat_t<8, true>(g, v.blocks_per_sm, keys, nw, L, mult, counts, st)
+                          : launch_fat_t<8, false>(g, v.blocks_per_sm, keys, nw, L, mult, counts, st); break;
+            default: v.agg ? launch_fat_t<4, true>(g, v.blocks_per_sm, keys, nw, L, mult, counts, st)
+                           : launch_fat_t<4, false>(g, v.blocks_per_sm, keys, nw, L, mult, counts, st); break;
+        }
+        return;
+    }
     const bool packed = v.packed && g->d_adj_packed != nullptr;
     switch (v.wpt) {
         case 1: launch_walk_w<1>(g, v, packed, c32, keys, nw, L, mult, counts, st); break;

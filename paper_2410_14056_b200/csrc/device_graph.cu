@@ -130,6 +130,7 @@ saba_cu_graph::~saba_cu_graph() {
     if (d_csr) saba_cu::pool_free(d_csr);
     if (d_adj) saba_cu::pool_free(d_adj);
     if (d_adj_packed) saba_cu::pool_free(d_adj_packed);
+    if (d_adj_fat) saba_cu::pool_free(d_adj_fat);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev2) cudaEventDestroy(ev2);

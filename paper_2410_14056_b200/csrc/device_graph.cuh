@@ -77,6 +77,13 @@ struct saba_cu_graph {
     // 3 x 21-bit ids per uint64 when n <= 2^21 (2.67 B/slot instead of 4):
     // shrinks the random-gather working set so more of it stays in L2
     uint64_t* d_adj_packed = nullptr;
+    // "fat" adjacency for the campaign: slot s holds its neighbour's
+    // {id, base, degree} in one uint64 (id | base << fat_idb | deg << fat_sh),
+    // so a walk step is one dependent gather instead of two. Built on first
+    // use when the three fields fit in 64 bits.
+    uint64_t* d_adj_fat = nullptr;
+    uint32_t fat_idb = 0, fat_sh = 0;
+    bool fat_tried = false;
     // campaign workspace (grow-only, reused across calls)
     saba_cu::DevBuf kv, off, keys, keys_alt, seg, cub_tmp, counts32;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
