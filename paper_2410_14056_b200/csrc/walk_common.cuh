@@ -11,6 +11,20 @@ __device__ __forceinline__ uint2 ldg_csr(const uint2* p) { return __ldg(p); }
 __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) { return __ldg(p); }
 __device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
 
+// Read-only gathers that do not allocate in L1: adjacency slots are touched
+// uniformly at random, so caching them in L1 only evicts the hot {base, deg}
+// records of hub vertices that L1 can actually keep.
+__device__ __forceinline__ uint64_t ldg_na_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg_na_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
 // Neighbour id at directed slot s. Packed: 3 x 21-bit fields per uint64.
 template <bool PACKED>
 __device__ __forceinline__ uint32_t adj_at(const uint32_t* __restrict__ adj,
@@ -18,10 +32,9 @@ __device__ __forceinline__ uint32_t adj_at(const uint32_t* __restrict__ adj,
     if constexpr (PACKED) {
         const uint32_t w = __umulhi(s, 0xAAAAAAABu) >> 1;  // s / 3 for s < 2^32
         const uint32_t r = s - 3 * w;
-        return uint32_t(__ldg(reinterpret_cast<const unsigned long long*>(packed) + w) >> (21 * r)) &
-               0x1FFFFFu;
+        return uint32_t(ldg_na_u64(packed + w) >> (21 * r)) & 0x1FFFFFu;
     } else {
-        return __ldg(adj + s);
+        return ldg_na_u32(adj + s);
     }
 }
 
