@@ -180,6 +180,94 @@ __global__ void __launch_bounds__(kWalkThreads)
     }
 }
 
+// K2 with hub-privatised counters. Visits are counted at DEPARTURE: the
+// record of x_{l-1} loaded at step l already says whether x_{l-1} is one of
+// the kHot highest-degree vertices (field y >> 18), whose counters live in
+// shared memory for the whole launch; every other visit is an L2 reduction.
+// x_0 is counted by gen_keys_kernel and x_{L-1} after the loop, so the
+// multiset of counted vertices equals the reference's (walker.hpp:216-232).
+constexpr uint32_t kHot = 16384;
+constexpr uint32_t kHotShift = 18;
+template <int WPT, bool PACKED, bool AGG>
+__global__ void __launch_bounds__(kWalkThreads)
+    walk_count_hot_kernel(const uint2* __restrict__ csr_hot, const uint32_t* __restrict__ adj,
+                          const uint64_t* __restrict__ adjp, const uint32_t* __restrict__ hot_vertex,
+                          uint32_t nhot, const uint64_t* __restrict__ keys, uint64_t nwalks,
+                          uint32_t L, uint64_t mult, unsigned long long* __restrict__ counts) {
+    extern __shared__ uint32_t hot_cnt[];
+    for (uint32_t i = threadIdx.x; i < nhot; i += blockDim.x) hot_cnt[i] = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t base = warp * 32 * WPT; base < nwalks; base += nwarps * 32 * WPT) {
+        uint32_t cur[WPT], seed[WPT];
+        bool act[WPT];
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {
+            const uint64_t i = base + uint64_t(r) * 32 + lane;
+            act[r] = i < nwalks;
+            const uint64_t k = act[r] ? __ldcs(reinterpret_cast<const unsigned long long*>(keys) + i) : 0;
+            cur[r] = uint32_t(k >> 32);
+            seed[r] = uint32_t(k);
+        }
+        for (uint32_t l = 1; l < L; ++l) {
+            uint2 rec[WPT];
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) rec[r] = act[r] ? ldg_csr(csr_hot + cur[r]) : make_uint2(0, 0);
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) {
+                const uint32_t deg = rec[r].y & ((1u << kHotShift) - 1);
+                const uint32_t slot = rec[r].y >> kHotShift;
+                if (l >= 2) {  // count the departing vertex x_{l-1}
+                    const bool hot = act[r] && slot != 0;
+                    if (hot) atomicAdd(hot_cnt + (slot - 1), 1u);
+                    if constexpr (AGG)
+                        warp_count_visit(counts, cur[r], act[r] && !hot, lane);
+                    else
+                        count_visit(counts, cur[r], act[r] && !hot);
+                }
+                const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
+                cur[r] = act[r] ? adj_at<PACKED>(adj, adjp, rec[r].x + scaled_index(raw, deg)) : 0u;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {  // the last vertex x_{L-1}
+            if constexpr (AGG)
+                warp_count_visit(counts, cur[r], act[r] && L > 1, lane);
+            else
+                count_visit(counts, cur[r], act[r] && L > 1);
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nhot; i += blockDim.x)
+        if (hot_cnt[i]) atomicAdd(counts + hot_vertex[i], (unsigned long long)hot_cnt[i]);
+}
+
+// Top-kHot vertices by degree get a shared-memory counter slot (packed into
+// the spare high bits of the degree field; needs max degree < 2^18).
+bool ensure_hot(saba_cu_graph* g) {
+    if (g->hot_tried) return g->d_csr_hot != nullptr;
+    g->hot_tried = true;
+    if (g->max_degree >= (1u << kHotShift) || g->n == 0) return false;
+    const uint32_t n = g->n, h = std::min(kHot, n);
+    std::vector<uint32_t> order(n);
+    for (uint32_t v = 0; v < n; ++v) order[v] = v;
+    auto deg = [&](uint32_t v) { return g->h_off[v + 1] - g->h_off[v]; };
+    std::partial_sort(order.begin(), order.begin() + h, order.end(), [&](uint32_t a, uint32_t b) {
+        return deg(a) != deg(b) ? deg(a) > deg(b) : a < b;
+    });
+    std::vector<uint2> rec(n);
+    for (uint32_t v = 0; v < n; ++v) rec[v] = make_uint2(g->h_off[v], deg(v));
+    for (uint32_t i = 0; i < h; ++i) rec[order[i]].y |= (i + 1) << kHotShift;
+    g->d_csr_hot = static_cast<uint2*>(pool_alloc(sizeof(uint2) * n));
+    g->d_hot_vertex = static_cast<uint32_t*>(pool_alloc(sizeof(uint32_t) * h));
+    SABA_CUDA_CHECK(cudaMemcpy(g->d_csr_hot, rec.data(), sizeof(uint2) * n, cudaMemcpyHostToDevice));
+    SABA_CUDA_CHECK(cudaMemcpy(g->d_hot_vertex, order.data(), sizeof(uint32_t) * h, cudaMemcpyHostToDevice));
+    g->hot_count = h;
+    return true;
+}
+
 bool ensure_fat(saba_cu_graph* g) {
     if (g->fat_tried) return g->d_adj_fat != nullptr;
     g->fat_tried = true;
@@ -216,6 +304,7 @@ struct WalkVariant {
     bool agg = true;
     int blocks_per_sm = 0;  // 0 = occupancy maximum
     int fat = -1;           // one-gather steps over the fat adjacency: 1 on, 0 off, -1 auto
+    int hot = -1;           // hub counters in shared memory: 1 on, 0 off, -1 auto
 };
 
 WalkVariant walk_variant() {
@@ -233,6 +322,7 @@ WalkVariant walk_variant() {
             w.agg = get("agg=", w.agg) != 0;
             w.blocks_per_sm = get("bps=", 0);
             w.fat = get("fat=", w.fat);
+            w.hot = get("hot=", w.hot);
         }
         return w;
     }();
@@ -279,6 +369,28 @@ void launch_fat_t(saba_cu_graph* g, int bps, const uint64_t* keys, uint64_t nw, 
     SABA_CUDA_CHECK(cudaGetLastError());
 }
 
+template <int WPT, bool P, bool A>
+bool launch_hot_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t L, uint64_t mult,
+                  void* counts, cudaStream_t st) {
+    auto k = walk_count_hot_kernel<WPT, P, A>;
+    const size_t smem = sizeof(uint32_t) * g->hot_count;
+    SABA_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int occ = 0;
+    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWalkThreads, smem));
+    if (occ < 1) return false;
+    const uint64_t blocks = uint64_t(g->sm_count) * occ;
+    // shared uint32 counters: a block can see at most ceil(nw / walks per
+    // round) * walks per block-round walks of L visits each
+    const uint64_t per_round = blocks * kWalkThreads * WPT;
+    const uint64_t per_block = (nw + per_round - 1) / per_round * kWalkThreads * WPT;
+    if (per_block * L >= (uint64_t(1) << 32)) return false;
+    k<<<uint32_t(blocks), kWalkThreads, smem, st>>>(g->d_csr_hot, g->d_adj, g->d_adj_packed,
+                                                    g->d_hot_vertex, g->hot_count, keys, nw, L, mult,
+                                                    static_cast<unsigned long long*>(counts));
+    SABA_CUDA_CHECK(cudaGetLastError());
+    return true;
+}
+
 void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, uint32_t L,
                  uint64_t mult, void* counts, cudaStream_t st) {
     const WalkVariant v = walk_variant();
@@ -298,6 +410,13 @@ void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, 
         return;
     }
     const bool packed = v.packed && g->d_adj_packed != nullptr;
+    if (v.hot != 0 && !c32 && ensure_hot(g)) {
+        const bool ok = packed ? (v.agg ? launch_hot_t<4, true, true>(g, keys, nw, L, mult, counts, st)
+                                        : launch_hot_t<4, true, false>(g, keys, nw, L, mult, counts, st))
+                               : (v.agg ? launch_hot_t<4, false, true>(g, keys, nw, L, mult, counts, st)
+                                        : launch_hot_t<4, false, false>(g, keys, nw, L, mult, counts, st));
+        if (ok) return;
+    }
     switch (v.wpt) {
         case 1: launch_walk_w<1>(g, v, packed, c32, keys, nw, L, mult, counts, st); break;
         case 2: launch_walk_w<2>(g, v, packed, c32, keys, nw, L, mult, counts, st); break;

@@ -131,6 +131,8 @@ saba_cu_graph::~saba_cu_graph() {
     if (d_adj) saba_cu::pool_free(d_adj);
     if (d_adj_packed) saba_cu::pool_free(d_adj_packed);
     if (d_adj_fat) saba_cu::pool_free(d_adj_fat);
+    if (d_csr_hot) saba_cu::pool_free(d_csr_hot);
+    if (d_hot_vertex) saba_cu::pool_free(d_hot_vertex);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev2) cudaEventDestroy(ev2);

@@ -84,6 +84,12 @@ struct saba_cu_graph {
     uint64_t* d_adj_fat = nullptr;
     uint32_t fat_idb = 0, fat_sh = 0;
     bool fat_tried = false;
+    // Hub-privatised counting: {base, degree | (hot slot + 1) << 18}; the
+    // top-degree vertices count their visits in shared memory.
+    uint2* d_csr_hot = nullptr;
+    uint32_t* d_hot_vertex = nullptr;  // slot -> vertex
+    uint32_t hot_count = 0;
+    bool hot_tried = false;
     // campaign workspace (grow-only, reused across calls)
     saba_cu::DevBuf kv, off, keys, keys_alt, seg, cub_tmp, counts32;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;

@@ -42,17 +42,19 @@ __device__ __forceinline__ uint32_t adj_at(const uint32_t* __restrict__ adj,
 // SABA bouquet sit on the same vertex in runs of adjacent lanes, so the head
 // of every run of equal `v` (found with one shuffle + ballot) issues a single
 // L2 reduction for the whole run. Divergent lanes degrade to one reduction
-// each. Active lanes must form a prefix of the warp; all 32 lanes must call.
+// each. Inactive lanes end a run (any active mask); all 32 lanes must call.
 template <class CT>
 __device__ __forceinline__ void warp_count_visit(CT* __restrict__ counts, uint32_t v, bool act,
                                                  uint32_t lane) {
     const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
     const uint32_t amask = __ballot_sync(0xffffffffu, act);
-    const bool head = act && (lane == 0 || prev != v);
+    const bool prev_act = lane > 0 && ((amask >> (lane - 1)) & 1u);
+    const bool head = act && (!prev_act || prev != v);
     const uint32_t heads = __ballot_sync(0xffffffffu, head);
     if (head) {
-        const uint32_t later = heads & ~((2u << lane) - 1u);  // heads strictly above lane
-        const uint32_t end = later ? uint32_t(__ffs(later) - 1) : uint32_t(__popc(amask));
+        // the run ends at the next head or the next inactive lane above this one
+        const uint32_t stops = (heads | ~amask) & ~((2u << lane) - 1u);
+        const uint32_t end = stops ? uint32_t(__ffs(stops) - 1) : 32u;
         atomicAdd(counts + v, static_cast<CT>(end - lane));
     }
 }
