@@ -17,6 +17,7 @@
 // thread advances WPT independent bouquet lanes so that several dependent
 // gather chains are in flight per thread (the walk is a pure random-gather
 // workload: no tensor cores).
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
@@ -246,24 +247,47 @@ __global__ void __launch_bounds__(kWalkThreads)
 
 // Top-kHot vertices by degree get a shared-memory counter slot (packed into
 // the spare high bits of the degree field; needs max degree < 2^18).
+__global__ void hot_keys_kernel(const uint2* __restrict__ csr, uint32_t n, uint32_t* __restrict__ key,
+                                uint32_t* __restrict__ id) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        key[v] = ~csr[v].y;  // ascending sort = descending degree
+        id[v] = v;
+    }
+}
+
+__global__ void hot_mark_kernel(const uint32_t* __restrict__ sorted_id, uint32_t h,
+                                uint2* __restrict__ csr_hot, uint32_t* __restrict__ hot_vertex) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < h; i += gridDim.x * blockDim.x) {
+        const uint32_t v = sorted_id[i];
+        hot_vertex[i] = v;
+        csr_hot[v].y |= (i + 1) << kHotShift;
+    }
+}
+
+// Built on the device (it sits on the end-to-end path of every new graph):
+// a stable radix sort by descending degree keeps ties in ascending id.
 bool ensure_hot(saba_cu_graph* g) {
     if (g->hot_tried) return g->d_csr_hot != nullptr;
     g->hot_tried = true;
     if (g->max_degree >= (1u << kHotShift) || g->n == 0) return false;
     const uint32_t n = g->n, h = std::min(kHot, n);
-    std::vector<uint32_t> order(n);
-    for (uint32_t v = 0; v < n; ++v) order[v] = v;
-    auto deg = [&](uint32_t v) { return g->h_off[v + 1] - g->h_off[v]; };
-    std::partial_sort(order.begin(), order.begin() + h, order.end(), [&](uint32_t a, uint32_t b) {
-        return deg(a) != deg(b) ? deg(a) > deg(b) : a < b;
-    });
-    std::vector<uint2> rec(n);
-    for (uint32_t v = 0; v < n; ++v) rec[v] = make_uint2(g->h_off[v], deg(v));
-    for (uint32_t i = 0; i < h; ++i) rec[order[i]].y |= (i + 1) << kHotShift;
+    DevBuf k0, k1, i0, i1, tmp;
+    cub::DoubleBuffer<uint32_t> keys(static_cast<uint32_t*>(k0.ensure(4 * size_t(n))),
+                                     static_cast<uint32_t*>(k1.ensure(4 * size_t(n))));
+    cub::DoubleBuffer<uint32_t> ids(static_cast<uint32_t*>(i0.ensure(4 * size_t(n))),
+                                    static_cast<uint32_t*>(i1.ensure(4 * size_t(n))));
+    const int blocks = int(std::min<uint32_t>((n + 255) / 256, uint32_t(g->sm_count) * 8));
+    hot_keys_kernel<<<blocks, 256>>>(g->d_csr, n, keys.Current(), ids.Current());
+    SABA_CUDA_CHECK(cudaGetLastError());
+    size_t tb = 0;
+    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, ids, int(n)));
+    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.ensure(tb), tb, keys, ids, int(n)));
     g->d_csr_hot = static_cast<uint2*>(pool_alloc(sizeof(uint2) * n));
     g->d_hot_vertex = static_cast<uint32_t*>(pool_alloc(sizeof(uint32_t) * h));
-    SABA_CUDA_CHECK(cudaMemcpy(g->d_csr_hot, rec.data(), sizeof(uint2) * n, cudaMemcpyHostToDevice));
-    SABA_CUDA_CHECK(cudaMemcpy(g->d_hot_vertex, order.data(), sizeof(uint32_t) * h, cudaMemcpyHostToDevice));
+    SABA_CUDA_CHECK(cudaMemcpy(g->d_csr_hot, g->d_csr, sizeof(uint2) * n, cudaMemcpyDeviceToDevice));
+    hot_mark_kernel<<<(h + 255) / 256, 256>>>(ids.Current(), h, g->d_csr_hot, g->d_hot_vertex);
+    SABA_CUDA_CHECK(cudaGetLastError());
+    SABA_CUDA_CHECK(cudaDeviceSynchronize());
     g->hot_count = h;
     return true;
 }
