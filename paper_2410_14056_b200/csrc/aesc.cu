@@ -538,14 +538,18 @@ __global__ void aesc_keygen(const WalkGroup* __restrict__ groups, const uint32_t
 // BITMAP: rho is non-zero only on the landing support; a 1-bit-per-vertex
 // check (64x smaller than rho, L2-resident) skips gathers of exact zeros
 // (adding +0.0 is the identity, so scores are unchanged).
-template <bool PACKED, int WPT, bool BITMAP>
+// FAT: slots carry the neighbour's {id, base, degree} (L2-resident graphs),
+// so a step is one dependent gather (plus the rho gather, which feeds nothing).
+template <bool PACKED, int WPT, bool BITMAP, bool FAT>
 __global__ void __launch_bounds__(256)
     aesc_walk_sorted(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                      uint32_t nwalks, const WalkGroup* __restrict__ groups,
                      const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
                      const uint64_t* __restrict__ adjp, const double* __restrict__ R, uint32_t n,
                      const uint32_t* __restrict__ bits, uint32_t words, uint64_t mult,
+                     const uint64_t* __restrict__ fat, uint32_t fat_idb, uint32_t fat_sh,
                      double* __restrict__ score) {
+    const uint64_t idmask = (uint64_t(1) << fat_idb) - 1, bmask = (uint64_t(1) << (fat_sh - fat_idb)) - 1;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -579,16 +583,29 @@ __global__ void __launch_bounds__(256)
             maxlen = max(maxlen, len[r]);
         }
         maxlen = __reduce_max_sync(0xffffffffu, maxlen);
-        for (uint32_t l = 1; l < maxlen; ++l) {
-            uint2 rec[WPT];
+        uint2 rec[WPT];
+        if constexpr (FAT) {
 #pragma unroll
-            for (int r = 0; r < WPT; ++r)
-                if (l < len[r]) rec[r] = ldg_csr(csr + cur[r]);
+            for (int r = 0; r < WPT; ++r) rec[r] = len[r] > 1 ? ldg_csr(csr + cur[r]) : make_uint2(0, 1);
+        }
+        for (uint32_t l = 1; l < maxlen; ++l) {
+            if constexpr (!FAT) {
+#pragma unroll
+                for (int r = 0; r < WPT; ++r)
+                    if (l < len[r]) rec[r] = ldg_csr(csr + cur[r]);
+            }
 #pragma unroll
             for (int r = 0; r < WPT; ++r)
                 if (l < len[r]) {
                     const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
-                    cur[r] = adj_at<PACKED>(adj, adjp, rec[r].x + scaled_index(raw, rec[r].y));
+                    if constexpr (FAT) {
+                        const uint64_t f = __ldg(reinterpret_cast<const unsigned long long*>(fat) + rec[r].x +
+                                                 scaled_index(raw, rec[r].y));
+                        cur[r] = uint32_t(f & idmask);
+                        rec[r] = make_uint2(uint32_t((f >> fat_idb) & bmask), uint32_t(f >> fat_sh));
+                    } else {
+                        cur[r] = adj_at<PACKED>(adj, adjp, rec[r].x + scaled_index(raw, rec[r].y));
+                    }
                 }
 #pragma unroll
             for (int r = 0; r < WPT; ++r)
@@ -940,15 +957,26 @@ int bits_for(uint32_t x) {
 
 // Walk phase: per chunk keygen -> radix sort (group, seed top bits) -> sorted
 // walks -> pair tiles; then the per-slot fold into g_hat.
+bool aesc_fat_enabled() {  // SABA_AESC_FAT=0 disables (default: on when L2-resident)
+    static const bool on = [] {
+        const char* e = getenv("SABA_AESC_FAT");
+        return !e || atoi(e) != 0;
+    }();
+    return on;
+}
+
 void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb, const double* R,
                const uint32_t* bits, uint64_t mult, double* g_hat_dev, uint32_t* launches) {
     const uint32_t words = (g->n + 31) / 32;
     if (tb.empty()) return;
     double* part = static_cast<double*>(st->partials.ensure(sizeof(double) * std::max(tb.ntiles, 1u)));
     const bool packed = g->d_adj_packed != nullptr;
+    // the fat adjacency is built (main thread) before any batch worker runs
+    const bool fat = g->d_adj_fat != nullptr && fat_fits_l2(g) && aesc_fat_enabled();
     constexpr int WPT = 4;
     int occ = 0;
-    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk_sorted<false, WPT, true>, 256, 0));
+    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk_sorted<false, WPT, true, true>,
+                                                                  256, 0));
     for (TileBuilder::Chunk& c : tb.chunks) {
         const uint32_t ng = uint32_t(c.groups.size()), nw = c.walks, nt = uint32_t(c.tiles.size());
         c.offs.push_back(nw);
@@ -972,14 +1000,16 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(t, tmp, keys, vals, int(nw), 0, end_bit, s));
         const int grid = int(std::min<uint64_t>((nw + 32 * WPT - 1) / (32 * WPT) * 32 / 256 + 1,
                                                 uint64_t(g->sm_count) * std::max(occ, 1)));
-#define SABA_WALK(P, B)                                                                           \
-    aesc_walk_sorted<P, WPT, B><<<grid, 256, 0, s>>>(keys.Current(), vals.Current(), nw, dg, g->d_csr, \
-                                                     g->d_adj, g->d_adj_packed, R, g->n, bits, words,  \
-                                                     mult, score)
-        if (packed) {
-            if (bits) SABA_WALK(true, true); else SABA_WALK(true, false);
+#define SABA_WALK(P, B, F)                                                                           \
+    aesc_walk_sorted<P, WPT, B, F><<<grid, 256, 0, s>>>(keys.Current(), vals.Current(), nw, dg, g->d_csr, \
+                                                        g->d_adj, g->d_adj_packed, R, g->n, bits, words,  \
+                                                        mult, g->d_adj_fat, g->fat_idb, g->fat_sh, score)
+        if (fat) {
+            if (bits) SABA_WALK(false, true, true); else SABA_WALK(false, false, true);
+        } else if (packed) {
+            if (bits) SABA_WALK(true, true, false); else SABA_WALK(true, false, false);
         } else {
-            if (bits) SABA_WALK(false, true); else SABA_WALK(false, false);
+            if (bits) SABA_WALK(false, true, false); else SABA_WALK(false, false, false);
         }
 #undef SABA_WALK
         SABA_CUDA_CHECK(cudaGetLastError());
@@ -1051,6 +1081,7 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
         const uint32_t n = g->n;
         const uint64_t m = g->m;
         for (uint64_t i = 0; i < source_count; ++i) check_arg(sources[i] < n, "source out of range");
+        if (fat_fits_l2(g) && aesc_fat_enabled()) ensure_fat(g);  // before the workers start
 
         Engine E(g);
         E.p = make_params(g, cfg->epsilon, cfg->delta, cfg->switch_depth_cap);

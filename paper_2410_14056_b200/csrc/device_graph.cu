@@ -41,7 +41,37 @@ __global__ void check_ids_kernel(const uint32_t* __restrict__ adj, uint64_t two_
         b |= adj[s] >= n;
     if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
 }
+// Fat adjacency: slot s -> adj[s] | base(adj[s]) << idb | degree(adj[s]) << sh.
+__global__ void build_fat_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                                 uint64_t two_m, uint32_t idb, uint32_t sh, uint64_t* __restrict__ fat) {
+    for (uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < two_m;
+         s += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t v = adj[s];
+        const uint2 r = csr[v];
+        fat[s] = uint64_t(v) | (uint64_t(r.x) << idb) | (uint64_t(r.y) << sh);
+    }
+}
 }  // namespace
+
+bool ensure_fat(saba_cu_graph* g) {
+    if (g->fat_tried) return g->d_adj_fat != nullptr;
+    g->fat_tried = true;
+    auto bits = [](uint64_t x) {  // bits to represent values in [0, x]
+        uint32_t b = 1;
+        while (b < 64 && (uint64_t(1) << b) <= x) ++b;
+        return b;
+    };
+    const uint32_t idb = bits(g->n ? g->n - 1 : 0), bb = bits(2 * g->m), db = bits(g->max_degree);
+    if (idb + bb + db > 64 || g->m == 0) return false;
+    g->fat_idb = idb;
+    g->fat_sh = idb + bb;
+    g->d_adj_fat = static_cast<uint64_t*>(pool_alloc(sizeof(uint64_t) * 2 * g->m));
+    build_fat_kernel<<<g->sm_count * 8, 256>>>(g->d_csr, g->d_adj, 2 * g->m, g->fat_idb, g->fat_sh,
+                                               g->d_adj_fat);
+    SABA_CUDA_CHECK(cudaGetLastError());
+    SABA_CUDA_CHECK(cudaDeviceSynchronize());
+    return true;
+}
 
 void ensure_pool(int device) {
     static bool done[64] = {};

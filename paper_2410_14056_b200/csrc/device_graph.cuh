@@ -100,6 +100,10 @@ struct saba_cu_graph {
 namespace saba_cu {
 const std::vector<uint32_t>& slot_edges(saba_cu_graph* g);
 const std::vector<uint32_t>& host_adj(saba_cu_graph* g);  // D2H once, then cached
+// Build the fat adjacency once (false if {id, base, degree} exceed 64 bits).
+bool ensure_fat(saba_cu_graph* g);
+// Fat adjacency is worth it while it stays comfortably L2-resident.
+inline bool fat_fits_l2(const saba_cu_graph* g) { return 16 * g->m <= (uint64_t(48) << 20); }
 constexpr uint32_t kPackBits = 21;
 constexpr uint32_t kPackMax = 1u << kPackBits;  // ids must be < 2^21 to pack
 }
