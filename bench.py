@@ -295,9 +295,42 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if world == 1 and args.workload == "cfg2" and not args.no_aesc:
+            out["aesc_cfg3"] = aesc_cfg3_summary(sb, args)
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def aesc_cfg3_summary(sb, args):
+    """BASELINE's second metric, reported beside the headline line: TGT+ AESC
+    wall time on config 3 (R-MAT s16 ef8 LCC, eps 0.1, delta 0.01, every
+    source), 1 warm-up + 1 timed run, with the reference's own CPU path timed
+    on a 64-source sample and extrapolated (bench.py --workload cfg3 is the
+    full-protocol measurement)."""
+    spec, eps, delta, _, cpu_sources = AESC_WORKLOADS["cfg3"]
+    g = make_aesc_graph(sb, spec)
+    cfg = sb.AescConfig(epsilon=eps, delta=delta)
+    sb.aesc(g, cfg)  # warm-up
+    t0 = time.perf_counter()
+    est = sb.aesc(g, cfg)
+    wall = time.perf_counter() - t0
+    res = {"workload": f"cfg3: R-MAT s16 ef8 LCC n={g.n} m={g.m} eps={eps} delta={delta}, all sources",
+           "seconds": wall, "unit": "s", "higher_is_better": False,
+           "walk_pairs": est.total_walk_pairs, "walk_steps": est.total_walk_steps,
+           "walk_steps_per_s": est.total_walk_steps / wall, "lambda_hat": est.plan.lambda_hat,
+           "tau": int(est.plan.max_tau)}
+    if not args.no_cpu_baseline:
+        from oracle.oracle import Reference, reference_available
+        if reference_available():
+            R = Reference()
+            r = R.aesc(R.from_csr(g.offsets, g.adjacency), epsilon=eps, delta=delta,
+                       sources=subset_sources(sb, g.n, cpu_sources))
+            res["cpu_baseline"] = {"value": r.plan_seconds + r.seconds * g.n / cpu_sources, "unit": "s",
+                                   "cores": R.max_threads(), "kind": "reference",
+                                   "sample": f"oracle/_ref aesc_source on {cpu_sources} sources, "
+                                             f"extrapolated x{g.n / cpu_sources:.1f}"}
+    return res
 
 
 AESC_WORKLOADS = {
@@ -449,6 +482,7 @@ def main():
     ap.add_argument("--mode", default="saba", choices=["saba", "hash"])
     ap.add_argument("--cpu-stride", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-aesc", action="store_true", help="skip the cfg3 AESC summary of the default run")
     args = ap.parse_args()
     if args.workload in AESC_WORKLOADS:
         if args.impl == "reference":
