@@ -285,7 +285,7 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MiB write, outside the events)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "walk_count_kernel (K2)", "kernel_ms": kern_ms,
+                         "kernel": "K2 walk kernel (walk_count_hot_kernel on cfg2)", "kernel_ms": kern_ms,
                          "step_share": kern_ms / ms_per_step,
                          "bytes_per_step": BYTES_PER_STEP, "peak_source": peak_src},
             "cpu_baseline": cpu,
