@@ -159,6 +159,16 @@ SABA_API int saba_cu_walk_campaign_device(saba_cu_graph* g, const saba_cu_campai
                                  uint64_t* counts_dev, void* stream, int timing,
                                  saba_cu_campaign_report* report);
 
+/* rng_stream (stream.hpp:29-83): the raw 32-bit pre-selection words
+ * seed ^ h(cur, l) of walks_per_vertex walks from each start, step-major per
+ * start (walk k's word of step l at index (l-1)*K + k of its start's block).
+ * selector: 1 = xor-mod, 2 = scaled (0 = the LCG baseline is rejected).
+ * *nwords = nstarts*K*(length-1); words_out may be NULL when length == 1. */
+SABA_API int saba_cu_rng_stream(saba_cu_graph* g, const uint32_t* starts, uint32_t nstarts,
+                                uint64_t walks_per_vertex, uint32_t length, int selector,
+                                uint64_t master_seed, uint64_t hash_multiplier,
+                                uint32_t* words_out, uint64_t* nwords);
+
 /* Branching statistics of the campaign's bouquets (BranchCollector,
  * walker.hpp:64-109 as driven by campaign_vertex_scaled, 430-449): bouquets
  * are `lanes` consecutive entries of each start vertex's (Saba: sorted) seed

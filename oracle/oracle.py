@@ -340,6 +340,17 @@ class Reference:
                                         _p(out, u64p), C.byref(sec), C.byref(steps)), "campaign")
         return out, sec.value, steps.value
 
+    def rng_stream(self, g, starts, K, L, selector=2, master=42, mult=DEFAULT_MULT):
+        st = np.ascontiguousarray(starts, np.uint32)
+        words = np.zeros(max(len(st) * K * max(L - 1, 0), 1), np.uint32)
+        nw = C.c_uint64()
+        fn = self.lib.ref_rng_stream
+        fn.argtypes = [C.c_void_p, u32p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int, C.c_uint64,
+                       C.c_uint64, u32p, u64p]
+        self._chk(fn(g.h, _p(st, u32p), len(st), K, L, selector, master, mult, _p(words, u32p),
+                     C.byref(nw)), "rng_stream")
+        return words[: nw.value]
+
     def campaign_stats(self, g, K, L, mode=3, lanes=8, threads=0, master=42, mult=DEFAULT_MULT):
         hist = np.zeros(lanes + 1, np.uint64)
         step = np.zeros(L - 1, np.uint64)

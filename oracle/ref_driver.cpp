@@ -6,6 +6,9 @@
 // is copied — every computation below is a call into the reference.
 #include "saba/aesc.hpp"
 #include "saba/gen.hpp"
+#include "saba/stream.hpp"
+
+#include <sstream>
 #include "saba/graph.hpp"
 #include "saba/walker.hpp"
 
@@ -403,5 +406,25 @@ REF_API int ref_aesc_sources(void* h, const RefAescConfig* c, const uint32_t* so
         }
         if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
         if (plan_seconds) *plan_seconds = std::chrono::duration<double>(t0 - p0).count();
+    });
+}
+
+// rng_stream (stream.hpp:29-83): raw little-endian pre-selection words.
+// selector: 0 naive, 1 xor, 2 scaled. Returns the number of words in *nwords.
+REF_API int ref_rng_stream(void* h, const uint32_t* starts, uint32_t nstarts, uint64_t K, uint32_t L,
+                           int selector, uint64_t master, uint64_t mult, uint32_t* words_out,
+                           uint64_t* nwords) {
+    return guarded([&] {
+        saba::StreamSpec spec;
+        spec.starts.assign(starts, starts + nstarts);
+        spec.walks_per_vertex = K;
+        spec.length = L;
+        spec.selector = static_cast<saba::SelectorKind>(selector);
+        spec.master_seed = master;
+        spec.hash = saba::HashSpec{mult};
+        std::ostringstream out;
+        *nwords = saba::rng_stream(*as_graph(h), spec, out);
+        const std::string bytes = out.str();
+        std::memcpy(words_out, bytes.data(), bytes.size());
     });
 }

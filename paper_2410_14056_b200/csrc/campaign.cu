@@ -513,6 +513,28 @@ __global__ void branch_stats_kernel(const uint2* __restrict__ csr, const uint32_
     }
 }
 
+// rng_stream (stream.hpp:29-83): the raw pre-selection word seed ^ h(cur, l)
+// of every step, merged step-major per start (word (l-1)*K + k of the start's
+// block). Thread per (start, k) walk. xor_mod = 1 selects raw % degree.
+__global__ void rng_stream_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                                  const uint32_t* __restrict__ starts, uint64_t total, uint64_t K,
+                                  uint32_t L, uint64_t master, uint64_t mult, int xor_mod,
+                                  uint32_t* __restrict__ words) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const uint64_t si = i / K, k = i - si * K;
+        uint32_t cur = starts[si];
+        const uint32_t seed = walk_seed(substream(master, cur), k);  // stream.hpp:45, 58
+        uint32_t* out = words + si * K * (L - 1) + k;
+        for (uint32_t l = 1; l < L; ++l) {
+            const uint2 rec = ldg_csr(csr + cur);
+            const uint32_t raw = seed ^ hash_state(mult, cur, l);
+            out[uint64_t(l - 1) * K] = raw;
+            cur = ldg_u32(adj + rec.x + (xor_mod ? raw % rec.y : scaled_index(raw, rec.y)));
+        }
+    }
+}
+
 // One thread per walk; materialises the path (random_walk, walker.hpp:283-302).
 __global__ void walk_paths_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
                                   const uint32_t* __restrict__ starts,
@@ -645,6 +667,40 @@ void fill_report(const saba_cu_graph* g, const saba_cu_campaign_config& c, uint6
 using namespace saba_cu;
 
 extern "C" {
+
+int saba_cu_rng_stream(saba_cu_graph* g, const uint32_t* starts, uint32_t nstarts,
+                       uint64_t walks_per_vertex, uint32_t length, int selector, uint64_t master,
+                       uint64_t mult, uint32_t* words_out, uint64_t* nwords) {
+    return guard([&] {
+        check_arg(g && nwords, "null argument");
+        // stream.hpp:32-36, same order and messages
+        check_arg(walks_per_vertex >= 1, "rng_stream: walks_per_vertex must be >= 1");
+        check_arg(length >= 1, "rng_stream: length must be >= 1");
+        check_arg(nstarts > 0 && starts, "rng_stream: no start vertices");
+        for (uint32_t i = 0; i < nstarts; ++i) {
+            check_arg(starts[i] < g->n, "start vertex out of range");
+            check_arg(length == 1 || g->h_off[starts[i] + 1] > g->h_off[starts[i]],
+                      "cannot walk from an isolated vertex");
+        }
+        check_arg(selector == 1 || selector == 2,
+                  "rng_stream: only the hashed selectors (xor, scaled) run on GPU");
+        *nwords = uint64_t(nstarts) * walks_per_vertex * (length - 1);
+        if (length == 1) return;
+        check_arg(words_out != nullptr, "null output");
+        DeviceScope scope(g->device);
+        DevBuf d_st, d_w;
+        d_st.ensure(sizeof(uint32_t) * nstarts);
+        d_w.ensure(sizeof(uint32_t) * *nwords);
+        SABA_CUDA_CHECK(cudaMemcpy(d_st.p, starts, sizeof(uint32_t) * nstarts, cudaMemcpyHostToDevice));
+        const uint64_t total = uint64_t(nstarts) * walks_per_vertex;
+        const int blocks = int(std::min<uint64_t>((total + 255) / 256, uint64_t(g->sm_count) * 8));
+        rng_stream_kernel<<<blocks, 256>>>(g->d_csr, g->d_adj, d_st.as<uint32_t>(), total,
+                                           walks_per_vertex, length, master, mult, selector == 1,
+                                           d_w.as<uint32_t>());
+        SABA_CUDA_CHECK(cudaGetLastError());
+        SABA_CUDA_CHECK(cudaMemcpy(words_out, d_w.p, sizeof(uint32_t) * *nwords, cudaMemcpyDeviceToHost));
+    });
+}
 
 int saba_cu_walk_paths(saba_cu_graph* g, const uint32_t* starts, const uint32_t* seeds,
                        uint64_t count, uint32_t length, uint64_t mult, uint32_t* paths_out) {

@@ -272,6 +272,22 @@ def run_walk_campaign(g: Graph, cfg: CampaignConfig, sink: VisitCountSink, *,
     return out
 
 
+def rng_stream(g: Graph, starts, walks_per_vertex: int = 1, length: int = 2,
+               selector: SelectorKind = SelectorKind.Scaled, master_seed: int = 42,
+               hash: HashSpec = HashSpec(), device: int = 0) -> bytes:
+    """stream.hpp:29-83: the raw pre-selection words seed ^ h(cur, l) as
+    little-endian bytes, step-major per start (Dieharder export)."""
+    st = np.ascontiguousarray(starts, np.uint32)
+    nw = C.c_uint64()
+    total = len(st) * max(walks_per_vertex, 0) * max(length - 1, 0)
+    words = np.zeros(max(total, 1), np.uint32)
+    L.check(L.lib().saba_cu_rng_stream(g.device_handle(device), L.ptr(st, L.u32p), len(st),
+                                       walks_per_vertex, length, int(selector), master_seed,
+                                       hash.multiplier, L.ptr(words, L.u32p), C.byref(nw)),
+            "rng_stream")
+    return words[: nw.value].astype("<u4").tobytes()
+
+
 def collect_branching(g: Graph, cfg: CampaignConfig, *, total_walks: int = 0, device: int = 0):
     """Branching statistics of the campaign's bouquets (walker.hpp:64-109,
     526-536) computed on the GPU (the reference's untimed stats pass,

@@ -98,6 +98,14 @@ def main():
         out[key + "/hist"], out[key + "/per_step"] = hist, step
         out[key + "/scalars"] = np.array([total, samples, mdeg, mean], np.float64)
 
+    # rng_stream (test_stream.cpp:75-104 and variants)
+    for gname, starts, K, L, sel, seed in (("petersen", [3], 16, 6, 2, 99), ("petersen", [3], 16, 6, 1, 99),
+                                           ("fig1", [0, 1, 2], 3, 4, 2, 7),
+                                           ("sf300_4_5", [5, 17, 250], 32, 8, 2, 7)):
+        w = R.rng_stream(G[gname], starts, K, L, sel, seed)
+        key = f"stream/{gname}/{'-'.join(map(str, starts))}/K{K}_L{L}_sel{sel}_s{seed}"
+        out[key] = w
+
     # walk budget (test_aesc.cpp:27 and a grid)
     wb = []
     for t in (1, 5, 13, 97):
