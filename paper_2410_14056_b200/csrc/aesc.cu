@@ -513,8 +513,11 @@ struct SlotWork {
     uint32_t pad;
 };
 
+// sb = seed bits in the key: just enough that a seed bucket holds about a
+// warp's worth of walks of the chunk's largest group (finer buckets would
+// not make warps more coherent, coarser ones would); <= kSeedBits.
 __global__ void aesc_keygen(const WalkGroup* __restrict__ groups, const uint32_t* __restrict__ walk_offs,
-                            uint32_t ngroups, uint32_t nwalks, uint32_t* __restrict__ keys,
+                            uint32_t ngroups, uint32_t nwalks, uint32_t sb, uint32_t* __restrict__ keys,
                             uint32_t* __restrict__ vals) {
     for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwalks; w += gridDim.x * blockDim.x) {
         uint32_t lo = 0, hi = ngroups;  // walk_offs[g] <= w < walk_offs[g+1]
@@ -528,7 +531,8 @@ __global__ void aesc_keygen(const WalkGroup* __restrict__ groups, const uint32_t
         const uint64_t k = G.k0 + (local - side * G.pairs);
         // walk seed counter_hash(edge_seed, 2k+side) >> 32 (aesc.hpp:485)
         const uint32_t seed = walk_seed(G.edge_seed, 2 * k + side);
-        keys[w] = (lo << kSeedBits) | (seed >> (32 - kSeedBits));
+        // (group, side, seed top bits): each (slot, side) is its own bouquet set
+        keys[w] = (((lo << 1) | side) << sb) | (seed >> (32 - sb));
         vals[w] = w;
     }
 }
@@ -547,7 +551,7 @@ __global__ void __launch_bounds__(256)
                      const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
                      const uint64_t* __restrict__ adjp, const double* __restrict__ R, uint32_t n,
                      const uint32_t* __restrict__ bits, uint32_t words, uint64_t mult,
-                     const uint64_t* __restrict__ fat, uint32_t fat_idb, uint32_t fat_sh,
+                     const uint64_t* __restrict__ fat, uint32_t fat_idb, uint32_t fat_sh, uint32_t sb,
                      double* __restrict__ score) {
     const uint64_t idmask = (uint64_t(1) << fat_idb) - 1, bmask = (uint64_t(1) << (fat_sh - fat_idb)) - 1;
     const uint32_t lane = threadIdx.x & 31;
@@ -571,7 +575,7 @@ __global__ void __launch_bounds__(256)
             bm[r] = bits;
             if (e < nwalks) {
                 w[r] = vals[e];
-                const WalkGroup G = groups[keys[e] >> kSeedBits];
+                const WalkGroup G = groups[keys[e] >> (sb + 1)];
                 const uint32_t local = w[r] - G.walk_off;
                 const uint32_t side = local >= G.pairs;
                 seed[r] = walk_seed(G.edge_seed, 2 * (G.k0 + (local - side * G.pairs)) + side);
@@ -915,6 +919,7 @@ struct TileBuilder {
         std::vector<uint32_t> offs;  // walk offsets + sentinel
         std::vector<PairTile> tiles;
         uint32_t walks = 0;
+        uint32_t max_pairs = 0;
     };
     std::vector<Chunk> chunks;
     std::vector<SlotWork> slots;
@@ -934,7 +939,7 @@ struct TileBuilder {
         for (uint64_t k0 = 0; k0 < n_req; k0 += kGroupPairs) {
             const uint32_t pairs = uint32_t(std::min<uint64_t>(kGroupPairs, n_req - k0));
             if (chunks.empty() || chunks.back().walks + 2ull * pairs > kChunkWalks ||
-                chunks.back().groups.size() >= (1u << (32 - kSeedBits)))
+                chunks.back().groups.size() >= (1u << (31 - kSeedBits)))
                 chunks.emplace_back();
             Chunk& c = chunks.back();
             const uint32_t gi = uint32_t(c.groups.size());
@@ -943,6 +948,7 @@ struct TileBuilder {
             for (uint32_t p0 = 0; p0 < pairs; p0 += kPairTile)
                 c.tiles.push_back({inv_n, gi, p0, std::min(kPairTile, pairs - p0), ntiles++});
             c.walks += 2 * pairs;
+            c.max_pairs = std::max(c.max_pairs, pairs);
         }
         w.t1 = ntiles;
         slots.push_back(w);
@@ -991,27 +997,40 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         cub::DoubleBuffer<uint32_t> vals(static_cast<uint32_t*>(st->vals[0].ensure(sizeof(uint32_t) * nw)),
                                          static_cast<uint32_t*>(st->vals[1].ensure(sizeof(uint32_t) * nw)));
         double* score = static_cast<double*>(st->score.ensure(sizeof(double) * nw));
-        aesc_keygen<<<g->sm_count * 8, 256, 0, s>>>(dg, doff, ng, nw, keys.Current(), vals.Current());
+        const uint32_t sb = uint32_t(std::min<int>(kSeedBits, std::max(4, bits_for(c.max_pairs / 32) + 1)));
+        aesc_keygen<<<g->sm_count * 8, 256, 0, s>>>(dg, doff, ng, nw, sb, keys.Current(), vals.Current());
         SABA_CUDA_CHECK(cudaGetLastError());
-        const int end_bit = int(kSeedBits) + std::max(1, bits_for(ng));
+        const int end_bit = int(sb) + 1 + std::max(1, bits_for(ng));
         size_t tmp = 0;
         SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, int(nw), 0, end_bit, s));
         void* t = st->sort_tmp.ensure(tmp);
         SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(t, tmp, keys, vals, int(nw), 0, end_bit, s));
         const int grid = int(std::min<uint64_t>((nw + 32 * WPT - 1) / (32 * WPT) * 32 / 256 + 1,
                                                 uint64_t(g->sm_count) * std::max(occ, 1)));
-#define SABA_WALK(P, B, F)                                                                           \
-    aesc_walk_sorted<P, WPT, B, F><<<grid, 256, 0, s>>>(keys.Current(), vals.Current(), nw, dg, g->d_csr, \
-                                                        g->d_adj, g->d_adj_packed, R, g->n, bits, words,  \
-                                                        mult, g->d_adj_fat, g->fat_idb, g->fat_sh, score)
+#define SABA_WALK_W(P, W, B, F)                                                                       \
+    aesc_walk_sorted<P, W, B, F><<<grid, 256, 0, s>>>(keys.Current(), vals.Current(), nw, dg, g->d_csr, \
+                                                      g->d_adj, g->d_adj_packed, R, g->n, bits, words,  \
+                                                      mult, g->d_adj_fat, g->fat_idb, g->fat_sh, sb, score)
+#define SABA_WALK(P, B, F) SABA_WALK_W(P, WPT, B, F)
+        static const int fat_wpt = [] {  // tuning knob SABA_AESC_WPT (fat path)
+            const char* e = getenv("SABA_AESC_WPT");
+            return e ? atoi(e) : 4;
+        }();
         if (fat) {
-            if (bits) SABA_WALK(false, true, true); else SABA_WALK(false, false, true);
+            if (fat_wpt == 8) {
+                if (bits) SABA_WALK_W(false, 8, true, true); else SABA_WALK_W(false, 8, false, true);
+            } else if (fat_wpt == 2) {
+                if (bits) SABA_WALK_W(false, 2, true, true); else SABA_WALK_W(false, 2, false, true);
+            } else {
+                if (bits) SABA_WALK(false, true, true); else SABA_WALK(false, false, true);
+            }
         } else if (packed) {
             if (bits) SABA_WALK(true, true, false); else SABA_WALK(true, false, false);
         } else {
             if (bits) SABA_WALK(false, true, false); else SABA_WALK(false, false, false);
         }
 #undef SABA_WALK
+#undef SABA_WALK_W
         SABA_CUDA_CHECK(cudaGetLastError());
         aesc_pair_reduce<<<int(std::min<uint32_t>(nt, g->sm_count * 8)), 256, 0, s>>>(dt, nt, dg, score, part);
         SABA_CUDA_CHECK(cudaGetLastError());
@@ -1109,7 +1128,11 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
         // A second worker pays off only when propagation is deep enough to
         // overlap with walks; shallow plans are walk-bound and two walk
         // phases would only contend for DRAM.
-        const int nworkers = plan.max_tau > 31 ? kWorkspaces : 1;
+        static const int workers_env = [] {  // SABA_AESC_WORKERS=1|2 overrides
+            const char* e = getenv("SABA_AESC_WORKERS");
+            return e ? std::max(1, std::min(kWorkspaces, atoi(e))) : 0;
+        }();
+        const int nworkers = workers_env ? workers_env : (plan.max_tau > 31 ? kWorkspaces : 1);
         std::vector<std::unique_ptr<Engine>> engines;
         engines.emplace_back(new Engine(std::move(E)));
         for (int w = 1; w < nworkers; ++w) {
