@@ -23,6 +23,11 @@ struct CudaError : std::runtime_error {
 inline void check_arg(bool ok, const char* msg) {
     if (!ok) throw ArgError(msg);
 }
+// const char* overload: a literal must not build a std::string per call
+// (these checks sit inside per-vertex loops on the end-to-end path)
+inline void check_data(bool ok, const char* msg) {
+    if (!ok) throw DataError(msg);
+}
 inline void check_data(bool ok, const std::string& msg) {
     if (!ok) throw DataError(msg);
 }

@@ -1,4 +1,5 @@
 // K0: device CSR upload and the handle lifecycle; library identification.
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -211,12 +212,24 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
         const cudaDeviceProp& prop = props[device];
         check_data(prop.major >= 10, "libsaba_cuda is built for sm_100a (B200)");
 
+        const bool trace = getenv("SABA_TRACE") != nullptr;
+        auto T0 = std::chrono::steady_clock::now();
+        auto lap = [&](const char* what) {
+            if (!trace) return;
+            cudaDeviceSynchronize();
+            const auto T1 = std::chrono::steady_clock::now();
+            fprintf(stderr, "[saba] graph_create %-12s %8.3f ms\n", what,
+                    std::chrono::duration<double, std::milli>(T1 - T0).count());
+            T0 = T1;
+        };
         auto g = std::make_unique<saba_cu_graph>();
         g->device = device;
         g->sm_count = prop.multiProcessorCount;
         g->n = n;
         g->m = two_m / 2;
+        lap("start");
         g->h_off.assign(offsets, offsets + n + 1);
+        lap("assign");
         uint32_t dmin = UINT32_MAX, dmax = 0;
         for (uint32_t v = 0; v < n; ++v) {
             check_data(offsets[v] <= offsets[v + 1], "offsets must be nondecreasing");
@@ -226,6 +239,7 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
         }
         g->min_degree = dmin;
         g->max_degree = dmax;
+        lap("host scan");
 
         ensure_pool(device);
         DevBuf d_offb, d_bad;
@@ -233,11 +247,13 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
         unsigned int* bad = static_cast<unsigned int*>(d_bad.ensure(sizeof(unsigned int)));
         g->d_csr = static_cast<uint2*>(pool_alloc(sizeof(uint2) * size_t(n)));
         g->d_adj = static_cast<uint32_t*>(pool_alloc(sizeof(uint32_t) * (two_m ? two_m : 1)));
+        lap("alloc");
         SABA_CUDA_CHECK(cudaMemcpy(d_off, offsets, sizeof(uint32_t) * (size_t(n) + 1),
                                    cudaMemcpyHostToDevice));
         if (two_m)
             SABA_CUDA_CHECK(cudaMemcpy(g->d_adj, adjacency, sizeof(uint32_t) * two_m,
                                        cudaMemcpyHostToDevice));
+        lap("h2d");
         pack_csr_kernel<<<(n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096, 256>>>(d_off, n, g->d_csr);
         SABA_CUDA_CHECK(cudaGetLastError());
         SABA_CUDA_CHECK(cudaMemset(bad, 0, sizeof(unsigned int)));
@@ -246,19 +262,19 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
         unsigned int h_bad = 0;
         SABA_CUDA_CHECK(cudaMemcpy(&h_bad, bad, sizeof(h_bad), cudaMemcpyDeviceToHost));
         check_data(h_bad == 0, "adjacency id out of range");
+        lap("check ids");
         if (n <= kPackMax && two_m) {
             const uint64_t words = (two_m + 2) / 3;
             g->d_adj_packed = static_cast<uint64_t*>(pool_alloc(sizeof(uint64_t) * words));
             pack_adj_kernel<<<g->sm_count * 8, 256>>>(g->d_adj, two_m, g->d_adj_packed);
             SABA_CUDA_CHECK(cudaGetLastError());
         }
-        if (const char* e = getenv("SABA_L2_FETCH")) {
-            SABA_CUDA_CHECK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(atoi(e))));
-        }
         SABA_CUDA_CHECK(cudaDeviceSynchronize());
+        lap("pack");
         SABA_CUDA_CHECK(cudaEventCreate(&g->ev0));
         SABA_CUDA_CHECK(cudaEventCreate(&g->ev1));
         SABA_CUDA_CHECK(cudaEventCreate(&g->ev2));
+        lap("events");
         *out = g.release();
     });
 }

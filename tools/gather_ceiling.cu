@@ -4,8 +4,10 @@
 // without the graph. Reports hops/s and 32 B-sector GB/s per working-set size,
 // with and without an extra RED.ADD per hop (the visit counter).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/gather_ceiling tools/gather_ceiling.cu
+//   tools/gather_ceiling [l2_fetch_granularity_bytes]
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t mixh(uint32_t x) {
@@ -57,9 +59,14 @@ double run(const uint32_t* a, uint32_t n, uint32_t* cnt, uint32_t ncnt, uint32_t
     return double(blocks) * 256 * WPT * hops / (ms * 1e-3);
 }
 
-int main() {
+int main(int argc, char** argv) {
     cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
-    printf("# %s SMs=%d L2=%d MB\n", p.name, p.multiProcessorCount, p.l2CacheSize >> 20);
+    // optional argv[1]: cudaLimitMaxL2FetchGranularity in bytes (0..128)
+    if (argc > 1) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(atoi(argv[1])));
+    size_t gran = 0;
+    cudaDeviceGetLimit(&gran, cudaLimitMaxL2FetchGranularity);
+    printf("# %s SMs=%d L2=%d MB  L2 fetch granularity %zu B\n", p.name, p.multiProcessorCount,
+           p.l2CacheSize >> 20, gran);
     uint32_t *a, *cnt, *sink;
     const uint64_t maxn = (1ull << 30) / 4 * 2;  // 2 GiB
     cudaMalloc(&a, maxn * 4); cudaMalloc(&cnt, 64 << 20); cudaMalloc(&sink, 4);
