@@ -172,18 +172,19 @@ __global__ void __launch_bounds__(kWalkThreads)
 
 // K2 with hub-privatised counters. Visits are counted at DEPARTURE: the
 // record of x_{l-1} loaded at step l already says whether x_{l-1} is one of
-// the kHot highest-degree vertices (field y >> 18), whose counters live in
+// the highest-degree vertices (field y >> shift), whose counters live in
 // shared memory for the whole launch; every other visit is an L2 reduction.
+// Large blocks (1024 threads) share one big table: at the register-limited
+// occupancy a block per SM holds up to ~56K hub counters instead of 3 x 16K.
 // x_0 is counted by gen_keys_kernel and x_{L-1} after the loop, so the
 // multiset of counted vertices equals the reference's (walker.hpp:216-232).
-constexpr uint32_t kHot = 16384;
-constexpr uint32_t kHotShift = 18;
-template <int WPT, bool PACKED, bool AGG>
-__global__ void __launch_bounds__(kWalkThreads)
+template <int WPT, bool PACKED, bool AGG, int THREADS>
+__global__ void __launch_bounds__(THREADS)
     walk_count_hot_kernel(const uint2* __restrict__ csr_hot, const uint32_t* __restrict__ adj,
                           const uint64_t* __restrict__ adjp, const uint32_t* __restrict__ hot_vertex,
-                          uint32_t nhot, const uint64_t* __restrict__ keys, uint64_t nwalks,
-                          uint32_t L, uint64_t mult, unsigned long long* __restrict__ counts) {
+                          uint32_t nhot, uint32_t shift, const uint64_t* __restrict__ keys,
+                          uint64_t nwalks, uint32_t L, uint64_t mult,
+                          unsigned long long* __restrict__ counts) {
     extern __shared__ uint32_t hot_cnt[];
     for (uint32_t i = threadIdx.x; i < nhot; i += blockDim.x) hot_cnt[i] = 0;
     __syncthreads();
@@ -207,8 +208,8 @@ __global__ void __launch_bounds__(kWalkThreads)
             for (int r = 0; r < WPT; ++r) rec[r] = act[r] ? ldg_csr(csr_hot + cur[r]) : make_uint2(0, 0);
 #pragma unroll
             for (int r = 0; r < WPT; ++r) {
-                const uint32_t deg = rec[r].y & ((1u << kHotShift) - 1);
-                const uint32_t slot = rec[r].y >> kHotShift;
+                const uint32_t deg = rec[r].y & ((1u << shift) - 1);
+                const uint32_t slot = rec[r].y >> shift;
                 if (l >= 2) {  // count the departing vertex x_{l-1}
                     const bool hot = act[r] && slot != 0;
                     if (hot) atomicAdd(hot_cnt + (slot - 1), 1u);
@@ -234,62 +235,6 @@ __global__ void __launch_bounds__(kWalkThreads)
         if (hot_cnt[i]) atomicAdd(counts + hot_vertex[i], (unsigned long long)hot_cnt[i]);
 }
 
-// Top-kHot vertices by degree get a shared-memory counter slot (packed into
-// the spare high bits of the degree field; needs max degree < 2^18).
-__global__ void hot_keys_kernel(const uint2* __restrict__ csr, uint32_t n, uint32_t* __restrict__ key,
-                                uint32_t* __restrict__ id) {
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        key[v] = ~csr[v].y;  // ascending sort = descending degree
-        id[v] = v;
-    }
-}
-
-__global__ void hot_mark_kernel(const uint32_t* __restrict__ sorted_id, uint32_t h,
-                                uint2* __restrict__ csr_hot, uint32_t* __restrict__ hot_vertex) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < h; i += gridDim.x * blockDim.x) {
-        const uint32_t v = sorted_id[i];
-        hot_vertex[i] = v;
-        csr_hot[v].y |= (i + 1) << kHotShift;
-    }
-}
-
-// Built on the device (it sits on the end-to-end path of every new graph):
-// a stable radix sort by descending degree keeps ties in ascending id.
-bool ensure_hot(saba_cu_graph* g) {
-    if (g->hot_tried) return g->d_csr_hot != nullptr;
-    g->hot_tried = true;
-    if (g->max_degree >= (1u << kHotShift) || g->n == 0) return false;
-    const uint32_t n = g->n, h = std::min(kHot, n);
-    DevBuf k0, k1, i0, i1, tmp;
-    cub::DoubleBuffer<uint32_t> keys(static_cast<uint32_t*>(k0.ensure(4 * size_t(n))),
-                                     static_cast<uint32_t*>(k1.ensure(4 * size_t(n))));
-    cub::DoubleBuffer<uint32_t> ids(static_cast<uint32_t*>(i0.ensure(4 * size_t(n))),
-                                    static_cast<uint32_t*>(i1.ensure(4 * size_t(n))));
-    const int blocks = int(std::min<uint32_t>((n + 255) / 256, uint32_t(g->sm_count) * 8));
-    hot_keys_kernel<<<blocks, 256>>>(g->d_csr, n, keys.Current(), ids.Current());
-    SABA_CUDA_CHECK(cudaGetLastError());
-    size_t tb = 0;
-    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, ids, int(n)));
-    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.ensure(tb), tb, keys, ids, int(n)));
-    g->d_csr_hot = static_cast<uint2*>(pool_alloc(sizeof(uint2) * n));
-    g->d_hot_vertex = static_cast<uint32_t*>(pool_alloc(sizeof(uint32_t) * h));
-    SABA_CUDA_CHECK(cudaMemcpy(g->d_csr_hot, g->d_csr, sizeof(uint2) * n, cudaMemcpyDeviceToDevice));
-    hot_mark_kernel<<<(h + 255) / 256, 256>>>(ids.Current(), h, g->d_csr_hot, g->d_hot_vertex);
-    SABA_CUDA_CHECK(cudaGetLastError());
-    SABA_CUDA_CHECK(cudaDeviceSynchronize());
-    g->hot_count = h;
-    return true;
-}
-
-
-__global__ void add_counts_kernel(const uint32_t* __restrict__ c32, uint32_t n,
-                                  unsigned long long* __restrict__ counts) {
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        const uint32_t c = c32[v];
-        if (c) counts[v] += c;
-    }
-}
-
 // Kernel variant (tuning knob; SABA_WALK_VARIANT="wpt=4,packed=1,c32=1,agg=1").
 struct WalkVariant {
     int wpt = 4;
@@ -299,6 +244,8 @@ struct WalkVariant {
     int blocks_per_sm = 0;  // 0 = occupancy maximum
     int fat = -1;           // one-gather steps over the fat adjacency: 1 on, 0 off, -1 auto
     int hot = -1;           // hub counters in shared memory: 1 on, 0 off, -1 auto
+    int hot_threads = 1024; // block size of the hub-counter kernel (256, 512, 1024)
+    int hot_count = 0;      // hub table entries (0 = as many as shared memory holds)
 };
 
 WalkVariant walk_variant() {
@@ -317,11 +264,86 @@ WalkVariant walk_variant() {
             w.blocks_per_sm = get("bps=", 0);
             w.fat = get("fat=", w.fat);
             w.hot = get("hot=", w.hot);
+            w.hot_threads = get("hthreads=", w.hot_threads);
+            w.hot_count = get("hcount=", w.hot_count);
         }
         return w;
     }();
     return v;
 }
+
+// The top vertices by degree get a shared-memory counter slot, packed into
+// the spare high bits of the degree field (hot_shift = bits of max degree).
+__global__ void hot_keys_kernel(const uint2* __restrict__ csr, uint32_t n, uint32_t* __restrict__ key,
+                                uint32_t* __restrict__ id) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        key[v] = ~csr[v].y;  // ascending sort = descending degree
+        id[v] = v;
+    }
+}
+
+__global__ void hot_mark_kernel(const uint32_t* __restrict__ sorted_id, uint32_t h, uint32_t shift,
+                                uint2* __restrict__ csr_hot, uint32_t* __restrict__ hot_vertex) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < h; i += gridDim.x * blockDim.x) {
+        const uint32_t v = sorted_id[i];
+        hot_vertex[i] = v;
+        csr_hot[v].y |= (i + 1) << shift;
+    }
+}
+
+// Built on the device (it sits on the end-to-end path of every new graph):
+// a stable radix sort by descending degree keeps ties in ascending id.
+bool ensure_hot(saba_cu_graph* g) {
+    if (g->hot_tried) return g->d_csr_hot != nullptr;
+    g->hot_tried = true;
+    if (g->n == 0) return false;
+    uint32_t shift = 1;
+    while (shift < 31 && (g->max_degree >> shift) != 0) ++shift;
+    const WalkVariant v = walk_variant();
+    g->hot_threads = v.hot_threads;
+    // shared table: 128 KB per SM. Shared memory and L1 share one SRAM and
+    // the L1 holds the in-flight gathers' lines; tables above ~160 KB starve
+    // it (cfg2: 23.2 ms at 128 KB, 31.3 ms at 176 KB, 66 ms at 226 KB;
+    // profiles/r01_walk_variant_sweep5_hot1024.txt)
+    const uint32_t cap = v.hot_count > 0
+                             ? uint32_t(v.hot_count)
+                             : uint32_t(std::min<size_t>((size_t(128) << 10) / sizeof(uint32_t) - 1,
+                                                         (g->smem_optin - 1024) / sizeof(uint32_t)) *
+                                        std::max(256, std::min(1024, g->hot_threads)) / 1024);
+    const uint32_t n = g->n;
+    const uint32_t h = std::min({n, (1u << (32 - shift)) - 1, cap});
+    if (h == 0) return false;
+    g->hot_shift = shift;
+    DevBuf k0, k1, i0, i1, tmp;
+    cub::DoubleBuffer<uint32_t> keys(static_cast<uint32_t*>(k0.ensure(4 * size_t(n))),
+                                     static_cast<uint32_t*>(k1.ensure(4 * size_t(n))));
+    cub::DoubleBuffer<uint32_t> ids(static_cast<uint32_t*>(i0.ensure(4 * size_t(n))),
+                                    static_cast<uint32_t*>(i1.ensure(4 * size_t(n))));
+    const int blocks = int(std::min<uint32_t>((n + 255) / 256, uint32_t(g->sm_count) * 8));
+    hot_keys_kernel<<<blocks, 256>>>(g->d_csr, n, keys.Current(), ids.Current());
+    SABA_CUDA_CHECK(cudaGetLastError());
+    size_t tb = 0;
+    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, ids, int(n)));
+    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.ensure(tb), tb, keys, ids, int(n)));
+    g->d_csr_hot = static_cast<uint2*>(pool_alloc(sizeof(uint2) * n));
+    g->d_hot_vertex = static_cast<uint32_t*>(pool_alloc(sizeof(uint32_t) * h));
+    SABA_CUDA_CHECK(cudaMemcpy(g->d_csr_hot, g->d_csr, sizeof(uint2) * n, cudaMemcpyDeviceToDevice));
+    hot_mark_kernel<<<(h + 255) / 256, 256>>>(ids.Current(), h, shift, g->d_csr_hot, g->d_hot_vertex);
+    SABA_CUDA_CHECK(cudaGetLastError());
+    SABA_CUDA_CHECK(cudaDeviceSynchronize());
+    g->hot_count = h;
+    return true;
+}
+
+
+__global__ void add_counts_kernel(const uint32_t* __restrict__ c32, uint32_t n,
+                                  unsigned long long* __restrict__ counts) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint32_t c = c32[v];
+        if (c) counts[v] += c;
+    }
+}
+
 
 template <int WPT, bool P, class CT, bool A>
 void launch_walk_t(const saba_cu_graph* g, int bps, const uint64_t* keys, uint64_t nw, uint32_t L,
@@ -363,26 +385,36 @@ void launch_fat_t(saba_cu_graph* g, int bps, const uint64_t* keys, uint64_t nw, 
     SABA_CUDA_CHECK(cudaGetLastError());
 }
 
-template <int WPT, bool P, bool A>
+template <int WPT, bool P, bool A, int T>
 bool launch_hot_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t L, uint64_t mult,
                   void* counts, cudaStream_t st) {
-    auto k = walk_count_hot_kernel<WPT, P, A>;
+    auto k = walk_count_hot_kernel<WPT, P, A, T>;
     const size_t smem = sizeof(uint32_t) * g->hot_count;
     SABA_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int occ = 0;
-    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWalkThreads, smem));
+    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, T, smem));
     if (occ < 1) return false;
     const uint64_t blocks = uint64_t(g->sm_count) * occ;
     // shared uint32 counters: a block can see at most ceil(nw / walks per
     // round) * walks per block-round walks of L visits each
-    const uint64_t per_round = blocks * kWalkThreads * WPT;
-    const uint64_t per_block = (nw + per_round - 1) / per_round * kWalkThreads * WPT;
+    const uint64_t per_round = blocks * T * WPT;
+    const uint64_t per_block = (nw + per_round - 1) / per_round * T * WPT;
     if (per_block * L >= (uint64_t(1) << 32)) return false;
-    k<<<uint32_t(blocks), kWalkThreads, smem, st>>>(g->d_csr_hot, g->d_adj, g->d_adj_packed,
-                                                    g->d_hot_vertex, g->hot_count, keys, nw, L, mult,
-                                                    static_cast<unsigned long long*>(counts));
+    k<<<uint32_t(blocks), T, smem, st>>>(g->d_csr_hot, g->d_adj, g->d_adj_packed, g->d_hot_vertex,
+                                         g->hot_count, g->hot_shift, keys, nw, L, mult,
+                                         static_cast<unsigned long long*>(counts));
     SABA_CUDA_CHECK(cudaGetLastError());
     return true;
+}
+
+template <bool P, bool A>
+bool launch_hot_p(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t L, uint64_t mult,
+                  void* counts, cudaStream_t st) {
+    switch (g->hot_threads) {
+        case 256: return launch_hot_t<4, P, A, 256>(g, keys, nw, L, mult, counts, st);
+        case 512: return launch_hot_t<4, P, A, 512>(g, keys, nw, L, mult, counts, st);
+        default: return launch_hot_t<4, P, A, 1024>(g, keys, nw, L, mult, counts, st);
+    }
 }
 
 void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, uint32_t L,
@@ -405,10 +437,10 @@ void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, 
     }
     const bool packed = v.packed && g->d_adj_packed != nullptr;
     if (v.hot != 0 && !c32 && ensure_hot(g)) {
-        const bool ok = packed ? (v.agg ? launch_hot_t<4, true, true>(g, keys, nw, L, mult, counts, st)
-                                        : launch_hot_t<4, true, false>(g, keys, nw, L, mult, counts, st))
-                               : (v.agg ? launch_hot_t<4, false, true>(g, keys, nw, L, mult, counts, st)
-                                        : launch_hot_t<4, false, false>(g, keys, nw, L, mult, counts, st));
+        const bool ok = packed ? (v.agg ? launch_hot_p<true, true>(g, keys, nw, L, mult, counts, st)
+                                        : launch_hot_p<true, false>(g, keys, nw, L, mult, counts, st))
+                               : (v.agg ? launch_hot_p<false, true>(g, keys, nw, L, mult, counts, st)
+                                        : launch_hot_p<false, false>(g, keys, nw, L, mult, counts, st));
         if (ok) return;
     }
     switch (v.wpt) {

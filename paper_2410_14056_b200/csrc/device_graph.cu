@@ -225,6 +225,7 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
         auto g = std::make_unique<saba_cu_graph>();
         g->device = device;
         g->sm_count = prop.multiProcessorCount;
+        g->smem_optin = prop.sharedMemPerBlockOptin;
         g->n = n;
         g->m = two_m / 2;
         lap("start");

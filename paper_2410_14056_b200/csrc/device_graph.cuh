@@ -65,6 +65,7 @@ struct AescState;  // aesc.cu
 struct saba_cu_graph {
     int device = 0;
     int sm_count = 148;
+    size_t smem_optin = 232448;  // sharedMemPerBlockOptin
     uint32_t n = 0;
     uint64_t m = 0;
     uint32_t max_degree = 0;
@@ -84,11 +85,13 @@ struct saba_cu_graph {
     uint64_t* d_adj_fat = nullptr;
     uint32_t fat_idb = 0, fat_sh = 0;
     bool fat_tried = false;
-    // Hub-privatised counting: {base, degree | (hot slot + 1) << 18}; the
-    // top-degree vertices count their visits in shared memory.
+    // Hub-privatised counting: {base, degree | (hot slot + 1) << hot_shift};
+    // the top-degree vertices count their visits in shared memory.
     uint2* d_csr_hot = nullptr;
     uint32_t* d_hot_vertex = nullptr;  // slot -> vertex
     uint32_t hot_count = 0;
+    uint32_t hot_shift = 18;  // degree bits below the slot field (fits max_degree)
+    int hot_threads = 1024;   // block size the hot table was sized for
     bool hot_tried = false;
     // campaign workspace (grow-only, reused across calls)
     saba_cu::DevBuf kv, off, keys, keys_alt, seg, cub_tmp, counts32;
