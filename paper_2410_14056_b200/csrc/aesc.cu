@@ -68,7 +68,7 @@ struct AescState {
     DevBuf ulist[2], ucount, flag, tflag, tlist, tcount;
     DevBuf col_src, col_tau, degsum[2], tt, ctrl;  // per-column state
     DevBuf tau_slot, slot_edge_d, g_hat, s_hat, rho1;
-    DevBuf tiles, slots, partials, groups, woffs, keys[2], vals[2], score, sort_tmp;
+    DevBuf tiles, slots, partials, groups, woffs, keys[2], vals[2], score, sort_tmp, gid;
     DevBuf heavy_rows, piece_off, pieces, part, part_mask;  // hub-row split (static per graph)
     uint32_t nheavy = 0, npieces = 0;
     bool heavy_built = false;
@@ -516,9 +516,12 @@ struct SlotWork {
 // sb = seed bits in the key: just enough that a seed bucket holds about a
 // warp's worth of walks of the chunk's largest group (finer buckets would
 // not make warps more coherent, coarser ones would); <= kSeedBits.
+// gid != nullptr: side-0 walks of one source (every slot of it starts at
+// v_i) share one bouquet keyed by the rho column, so they sort together
+// across slots; gid[w] then records each walk's group.
 __global__ void aesc_keygen(const WalkGroup* __restrict__ groups, const uint32_t* __restrict__ walk_offs,
                             uint32_t ngroups, uint32_t nwalks, uint32_t sb, uint32_t* __restrict__ keys,
-                            uint32_t* __restrict__ vals) {
+                            uint32_t* __restrict__ vals, uint32_t* __restrict__ gid) {
     for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwalks; w += gridDim.x * blockDim.x) {
         uint32_t lo = 0, hi = ngroups;  // walk_offs[g] <= w < walk_offs[g+1]
         while (hi - lo > 1) {
@@ -531,8 +534,14 @@ __global__ void aesc_keygen(const WalkGroup* __restrict__ groups, const uint32_t
         const uint64_t k = G.k0 + (local - side * G.pairs);
         // walk seed counter_hash(edge_seed, 2k+side) >> 32 (aesc.hpp:485)
         const uint32_t seed = walk_seed(G.edge_seed, 2 * k + side);
-        // (group, side, seed top bits): each (slot, side) is its own bouquet set
-        keys[w] = (((lo << 1) | side) << sb) | (seed >> (32 - sb));
+        if (gid) {
+            const uint32_t seg = side ? kCols + lo : G.col;
+            keys[w] = (seg << sb) | (seed >> (32 - sb));
+            gid[w] = lo;
+        } else {
+            // (group, side, seed top bits): each (slot, side) is its own bouquet set
+            keys[w] = (((lo << 1) | side) << sb) | (seed >> (32 - sb));
+        }
         vals[w] = w;
     }
 }
@@ -552,37 +561,41 @@ __global__ void __launch_bounds__(256)
                      const uint64_t* __restrict__ adjp, const double* __restrict__ R, uint32_t n,
                      const uint32_t* __restrict__ bits, uint32_t words, uint64_t mult,
                      const uint64_t* __restrict__ fat, uint32_t fat_idb, uint32_t fat_sh, uint32_t sb,
-                     double* __restrict__ score) {
+                     const uint32_t* __restrict__ gid, double* __restrict__ score) {
+    // Software-pipelined score side: the walk chain (csr -> adj, or one fat
+    // gather) is the only dependency carried from step to step; the support
+    // bit of x_l is loaded right after x_l is known, the rho gather of x_l is
+    // issued at step l+1 and added at step l+2, so neither stalls the chain.
+    // Additions still happen in step order (aesc.hpp:491-493).
     const uint64_t idmask = (uint64_t(1) << fat_idb) - 1, bmask = (uint64_t(1) << (fat_sh - fat_idb)) - 1;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     for (uint64_t base = uint64_t(warp) * 32 * WPT; base < nwalks; base += uint64_t(nwarps) * 32 * WPT) {
-        uint32_t cur[WPT], seed[WPT], len[WPT], w[WPT];
-        const double* rho[WPT];
-        const uint32_t* bm[WPT];
-        double sc[WPT];
+        uint32_t cur[WPT], seed[WPT], len[WPT], col[WPT], bcol[WPT], bw[WPT];
+        double sc[WPT], rv[WPT];
         uint32_t maxlen = 1;
 #pragma unroll
         for (int r = 0; r < WPT; ++r) {
             const uint64_t e = base + uint64_t(r) * 32 + lane;
             len[r] = 1;
             sc[r] = 0.0;
-            w[r] = 0xffffffffu;
+            rv[r] = 0.0;
+            bw[r] = 0;
             cur[r] = 0;
             seed[r] = 0;
-            rho[r] = R;
-            bm[r] = bits;
+            col[r] = 0;
+            bcol[r] = 0;
             if (e < nwalks) {
-                w[r] = vals[e];
-                const WalkGroup G = groups[keys[e] >> (sb + 1)];
-                const uint32_t local = w[r] - G.walk_off;
+                const uint32_t w = vals[e];
+                const WalkGroup G = groups[gid ? __ldg(gid + w) : keys[e] >> (sb + 1)];
+                const uint32_t local = w - G.walk_off;
                 const uint32_t side = local >= G.pairs;
                 seed[r] = walk_seed(G.edge_seed, 2 * (G.k0 + (local - side * G.pairs)) + side);
                 cur[r] = side ? G.vj : G.vi;
                 len[r] = G.len;
-                rho[r] = R + size_t(G.col) * n;
-                bm[r] = bits + size_t(G.col) * words;
+                col[r] = G.col * n;  // 32-bit element offsets: kCols * n < 2^32 (checked by the host)
+                bcol[r] = G.col * words;
             }
             maxlen = max(maxlen, len[r]);
         }
@@ -592,11 +605,18 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
             for (int r = 0; r < WPT; ++r) rec[r] = len[r] > 1 ? ldg_csr(csr + cur[r]) : make_uint2(0, 1);
         }
-        for (uint32_t l = 1; l < maxlen; ++l) {
-            if constexpr (!FAT) {
+        for (uint32_t l = 1; l < maxlen + 2; ++l) {
+            if constexpr (!FAT) {  // critical load of step l first
 #pragma unroll
                 for (int r = 0; r < WPT; ++r)
                     if (l < len[r]) rec[r] = ldg_csr(csr + cur[r]);
+            }
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) {
+                sc[r] += rv[r];  // step l-2 (0.0 when it was not a support step)
+                // step l-1: cur is still x_{l-1}; bw holds its support bit
+                const bool hit = BITMAP ? ((bw[r] >> (cur[r] & 31)) & 1u) != 0 : bw[r] != 0;
+                rv[r] = hit ? __ldg(R + (col[r] + cur[r])) : 0.0;  // col[r] = column * n
             }
 #pragma unroll
             for (int r = 0; r < WPT; ++r)
@@ -610,20 +630,19 @@ __global__ void __launch_bounds__(256)
                     } else {
                         cur[r] = adj_at<PACKED>(adj, adjp, rec[r].x + scaled_index(raw, rec[r].y));
                     }
-                }
-#pragma unroll
-            for (int r = 0; r < WPT; ++r)
-                if (l < len[r]) {
-                    if constexpr (BITMAP) {
-                        if ((__ldg(bm[r] + (cur[r] >> 5)) >> (cur[r] & 31)) & 1u) sc[r] += __ldg(rho[r] + cur[r]);
-                    } else {
-                        sc[r] += __ldg(rho[r] + cur[r]);
-                    }
+                    if constexpr (BITMAP)
+                        bw[r] = __ldg(bits + (bcol[r] + (cur[r] >> 5)));
+                    else
+                        bw[r] = 1u;
+                } else {
+                    bw[r] = 0u;
                 }
         }
 #pragma unroll
-        for (int r = 0; r < WPT; ++r)
-            if (w[r] != 0xffffffffu) score[w[r]] = sc[r];
+        for (int r = 0; r < WPT; ++r) {  // walk ids are re-read (one register less per walk)
+            const uint64_t e = base + uint64_t(r) * 32 + lane;
+            if (e < nwalks) score[vals[e]] = sc[r];
+        }
     }
 }
 
@@ -713,6 +732,9 @@ struct Engine {
         }
         s = st->stream;
         const uint32_t n = g->n;
+        // the walk kernel addresses the rho block with 32-bit element offsets
+        check_data(uint64_t(kCols) * n < (uint64_t(1) << 32),
+                   "graph too large for the AESC batch layout (n must be < 2^26)");
         if (st->n_cap < n) {
             const size_t rows = size_t(n) * kCols;
             for (int b = 0; b < 2; ++b) {
@@ -920,6 +942,7 @@ struct TileBuilder {
         std::vector<PairTile> tiles;
         uint32_t walks = 0;
         uint32_t max_pairs = 0;
+        uint32_t col_pairs[kCols] = {};  // side-0 walks per source column
     };
     std::vector<Chunk> chunks;
     std::vector<SlotWork> slots;
@@ -949,6 +972,7 @@ struct TileBuilder {
                 c.tiles.push_back({inv_n, gi, p0, std::min(kPairTile, pairs - p0), ntiles++});
             c.walks += 2 * pairs;
             c.max_pairs = std::max(c.max_pairs, pairs);
+            c.col_pairs[col] += pairs;
         }
         w.t1 = ntiles;
         slots.push_back(w);
@@ -997,10 +1021,19 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         cub::DoubleBuffer<uint32_t> vals(static_cast<uint32_t*>(st->vals[0].ensure(sizeof(uint32_t) * nw)),
                                          static_cast<uint32_t*>(st->vals[1].ensure(sizeof(uint32_t) * nw)));
         double* score = static_cast<double*>(st->score.ensure(sizeof(double) * nw));
-        const uint32_t sb = uint32_t(std::min<int>(kSeedBits, std::max(4, bits_for(c.max_pairs / 32) + 1)));
-        aesc_keygen<<<g->sm_count * 8, 256, 0, s>>>(dg, doff, ng, nw, sb, keys.Current(), vals.Current());
+        static const bool merge = [] {  // SABA_AESC_MERGE=1: per-source side-0 bouquets
+            const char* e = getenv("SABA_AESC_MERGE");
+            return e && atoi(e) != 0;
+        }();
+        uint32_t max_seg = c.max_pairs;
+        if (merge)
+            for (uint32_t cp : c.col_pairs) max_seg = std::max(max_seg, cp);
+        uint32_t* gid = merge ? static_cast<uint32_t*>(st->gid.ensure(sizeof(uint32_t) * nw)) : nullptr;
+        const uint32_t sb = uint32_t(std::min<int>(kSeedBits, std::max(4, bits_for(max_seg / 32) + 1)));
+        aesc_keygen<<<g->sm_count * 8, 256, 0, s>>>(dg, doff, ng, nw, sb, keys.Current(), vals.Current(), gid);
         SABA_CUDA_CHECK(cudaGetLastError());
-        const int end_bit = int(sb) + 1 + std::max(1, bits_for(ng));
+        const int end_bit = merge ? int(sb) + std::max(1, bits_for(kCols + ng))
+                                  : int(sb) + 1 + std::max(1, bits_for(ng));
         size_t tmp = 0;
         SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, int(nw), 0, end_bit, s));
         void* t = st->sort_tmp.ensure(tmp);
@@ -1010,7 +1043,7 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
 #define SABA_WALK_W(P, W, B, F)                                                                       \
     aesc_walk_sorted<P, W, B, F><<<grid, 256, 0, s>>>(keys.Current(), vals.Current(), nw, dg, g->d_csr, \
                                                       g->d_adj, g->d_adj_packed, R, g->n, bits, words,  \
-                                                      mult, g->d_adj_fat, g->fat_idb, g->fat_sh, sb, score)
+                                                      mult, g->d_adj_fat, g->fat_idb, g->fat_sh, sb, gid, score)
 #define SABA_WALK(P, B, F) SABA_WALK_W(P, WPT, B, F)
         static const int fat_wpt = [] {  // tuning knob SABA_AESC_WPT (fat path)
             const char* e = getenv("SABA_AESC_WPT");
