@@ -1034,10 +1034,13 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         SABA_CUDA_CHECK(cudaGetLastError());
         const int end_bit = merge ? int(sb) + std::max(1, bits_for(kCols + ng))
                                   : int(sb) + 1 + std::max(1, bits_for(ng));
-        size_t tmp = 0;
-        SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, int(nw), 0, end_bit, s));
-        void* t = st->sort_tmp.ensure(tmp);
-        SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(t, tmp, keys, vals, int(nw), 0, end_bit, s));
+        static const bool nosort = getenv("SABA_AESC_NOSORT") != nullptr;  // experiment knob
+        if (!nosort) {
+            size_t tmp = 0;
+            SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, int(nw), 0, end_bit, s));
+            void* t = st->sort_tmp.ensure(tmp);
+            SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(t, tmp, keys, vals, int(nw), 0, end_bit, s));
+        }
         const int grid = int(std::min<uint64_t>((nw + 32 * WPT - 1) / (32 * WPT) * 32 / 256 + 1,
                                                 uint64_t(g->sm_count) * std::max(occ, 1)));
 #define SABA_WALK_W(P, W, B, F)                                                                       \
