@@ -71,6 +71,8 @@ struct AescState {
     DevBuf tiles, slots, partials, groups, woffs, keys[2], vals[2], score, sort_tmp, gid;
     DevBuf heavy_rows, piece_off, pieces, part, part_mask;  // hub-row split (static per graph)
     uint32_t nheavy = 0, npieces = 0;
+    DevBuf light_order;  // light rows by descending degree (dense depths)
+    uint32_t nlight = 0;
     bool heavy_built = false;
     cudaStream_t stream = nullptr;
     uint64_t* h_ctrl = nullptr;  // pinned mirror of the control block
@@ -90,7 +92,7 @@ void release_aesc_state(saba_cu_graph* g) {
 namespace {
 
 // Control block (device): active mask, frozen-at-this-depth mask, dense flag.
-enum { kActive = 0, kFrozenNow = 1, kDense = 2, kDenseReq = 3, kDepth = 4, kCtrlWords = 8 };
+enum { kActive = 0, kFrozenNow = 1, kDense = 2, kDenseReq = 3, kDepth = 4, kRowNext = 5, kCtrlWords = 8 };
 
 struct AescParams {
     double eps, delta, log_term;  // log_term = log(4m/delta) (aesc.hpp:109)
@@ -206,6 +208,7 @@ __global__ void aesc_check(uint32_t* __restrict__ ucount_next, const uint32_t* _
         // depth sees the same mode
         if (ctrl[kDenseReq]) ctrl[kDense] = 1;
         ctrl[kDepth] = l + 1;
+        ctrl[kRowNext] = 0;  // dense pull: next row of the degree-ordered list
         *ucount_next = 0;
     }
 }
@@ -339,6 +342,10 @@ __device__ __forceinline__ void flush_degsum(unsigned long long* sm, unsigned lo
     if (threadIdx.x < kCols && sm[threadIdx.x]) atomicAdd(degsum_next + threadIdx.x, sm[threadIdx.x]);
 }
 
+struct HeavyPiece {
+    uint32_t row, begin, end, pad;
+};
+
 // Pull SpMM over the candidate rows (sparse) or all rows (dense) with at
 // most kHeavy neighbours. Warp per row, lane = columns {2 lane, 2 lane + 1}.
 __global__ void __launch_bounds__(256)
@@ -347,16 +354,47 @@ __global__ void __launch_bounds__(256)
               double* __restrict__ Pn, double* __restrict__ Qn, unsigned long long* __restrict__ Mn,
               const uint32_t* __restrict__ ulist_next, const uint32_t* __restrict__ ucount_next,
               uint32_t* __restrict__ flag, unsigned long long* __restrict__ degsum_next,
-              unsigned long long* __restrict__ ctrl, uint32_t n) {
+              unsigned long long* __restrict__ ctrl, uint32_t n,
+              const uint32_t* __restrict__ light_order, uint32_t nlight,
+              const HeavyPiece* __restrict__ pieces, uint32_t npieces, double* __restrict__ part,
+              unsigned long long* __restrict__ part_mask) {
     __shared__ unsigned long long bds[kCols];
     const unsigned long long active = ctrl[kActive];
     if (!active) return;
     if (threadIdx.x < kCols) bds[threadIdx.x] = 0;
     __syncthreads();
     const bool dense = ctrl[kDense] != 0;
-    const uint32_t rows = dense ? n : *ucount_next;
     const uint32_t lane = threadIdx.x & 31;
     unsigned long long ds0 = 0, ds1 = 0;
+    if (dense && light_order) {
+        // dense depths: hub-row pieces, then light rows in descending degree
+        // order, handed out one at a time (longest first), so no warp is
+        // left with a long tail; aesc_pull_combine folds the pieces after
+        for (;;) {
+            uint32_t i = 0;
+            if (lane == 0) i = uint32_t(atomicAdd(ctrl + kRowNext, 1ull));
+            i = __shfl_sync(0xffffffffu, i, 0);
+            if (i >= npieces + nlight) break;
+            if (i < npieces) {
+                const HeavyPiece pc = pieces[i];
+                double a0 = 0.0, a1 = 0.0;
+                unsigned long long mask = 0;
+                pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, a0, a1, mask);
+                reinterpret_cast<double2*>(part + size_t(i) * kCols)[lane] = make_double2(a0, a1);
+                if (lane == 0) part_mask[i] = mask;
+                continue;
+            }
+            const uint32_t x = light_order[i - npieces];
+            const uint2 r = csr[x];
+            double a0 = 0.0, a1 = 0.0;
+            unsigned long long mask = 0;
+            pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, a0, a1, mask);
+            pull_store(x, r.y, a0, a1, mask, active, lane, Pn, Qn, Mn, ds0, ds1);
+        }
+        flush_degsum(bds, ds0, ds1, lane, degsum_next);
+        return;
+    }
+    const uint32_t rows = dense ? n : *ucount_next;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < rows;
          i += (gridDim.x * blockDim.x) >> 5) {
         const uint32_t x = dense ? i : ulist_next[i];
@@ -373,9 +411,6 @@ __global__ void __launch_bounds__(256)
     if (!dense && blockIdx.x == 0 && threadIdx.x == 0 && rows > n / 4) ctrl[kDenseReq] = 1;
 }
 
-struct HeavyPiece {
-    uint32_t row, begin, end, pad;
-};
 
 // Warp per piece of a heavy row that is a candidate at this depth.
 __global__ void __launch_bounds__(256)
@@ -383,9 +418,10 @@ __global__ void __launch_bounds__(256)
                      const uint32_t* __restrict__ adj, const double* __restrict__ Qc,
                      const unsigned long long* __restrict__ Mc, const uint32_t* __restrict__ flag,
                      double* __restrict__ part, unsigned long long* __restrict__ part_mask,
-                     const unsigned long long* __restrict__ ctrl) {
+                     const unsigned long long* __restrict__ ctrl, uint32_t dynamic) {
     if (!ctrl[kActive]) return;
     const bool dense = ctrl[kDense] != 0;
+    if (dense && dynamic) return;  // aesc_pull takes the pieces in dense depths
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < npieces;
          i += (gridDim.x * blockDim.x) >> 5) {
@@ -783,6 +819,15 @@ struct Engine {
                                         sizeof(HeavyPiece) * pcs.size(), cudaMemcpyHostToDevice, s));
         buf<double>(st->part, size_t(pcs.size()) * kCols);
         buf<uint64_t>(st->part_mask, pcs.size());
+        std::vector<uint32_t> light;
+        light.reserve(g->n);
+        for (uint32_t v = 0; v < g->n; ++v)
+            if (g->h_off[v + 1] - g->h_off[v] <= kHeavy) light.push_back(v);
+        std::stable_sort(light.begin(), light.end(), [&](uint32_t a, uint32_t b) { return deg(a) > deg(b); });
+        st->nlight = getenv("SABA_PULL_STATIC") ? 0u : uint32_t(light.size());
+        if (!light.empty())
+            SABA_CUDA_CHECK(cudaMemcpyAsync(buf<uint32_t>(st->light_order, light.size()), light.data(),
+                                            sizeof(uint32_t) * light.size(), cudaMemcpyHostToDevice, s));
         SABA_CUDA_CHECK(cudaStreamSynchronize(s));  // host vectors go out of scope
         st->heavy_built = true;
     }
@@ -858,17 +903,23 @@ struct Engine {
                                           st->bits.as<uint32_t>(), words());
             aesc_expand<<<grid, 256, 0, s>>>(csr, adj, M[cur], UL[cur], UC + cur, UL[cur ^ 1],
                                              UC + (cur ^ 1), flag, tflag, tlist, tcount, ctrl);
-            if (st->npieces) {
+            // sparse depths: pieces of candidate hub rows; dense depths: the
+            // pull kernel takes the pieces into its dynamic work list
+            if (st->npieces)
                 aesc_pull_pieces<<<grid, 256, 0, s>>>(st->pieces.as<HeavyPiece>(), st->npieces, adj,
                                                       Q[cur], M[cur], flag, st->part.as<double>(),
-                                                      st->part_mask.as<unsigned long long>(), ctrl);
+                                                      st->part_mask.as<unsigned long long>(), ctrl,
+                                                      st->nlight);
+            aesc_pull<<<grid_pull, 256, 0, s>>>(csr, adj, Q[cur], M[cur], P[cur ^ 1], Q[cur ^ 1], M[cur ^ 1],
+                                           UL[cur ^ 1], UC + (cur ^ 1), flag, DS[cur ^ 1], ctrl, n,
+                                           st->nlight ? st->light_order.as<uint32_t>() : nullptr, st->nlight,
+                                           st->pieces.as<HeavyPiece>(), st->npieces, st->part.as<double>(),
+                                           st->part_mask.as<unsigned long long>());
+            if (st->npieces)
                 aesc_pull_combine<<<grid_comb, 256, 0, s>>>(
                     st->heavy_rows.as<uint32_t>(), st->piece_off.as<uint32_t>(), st->nheavy, csr,
                     st->part.as<double>(), st->part_mask.as<unsigned long long>(), P[cur ^ 1],
                     Q[cur ^ 1], M[cur ^ 1], flag, DS[cur ^ 1], ctrl);
-            }
-            aesc_pull<<<grid_pull, 256, 0, s>>>(csr, adj, Q[cur], M[cur], P[cur ^ 1], Q[cur ^ 1], M[cur ^ 1],
-                                           UL[cur ^ 1], UC + (cur ^ 1), flag, DS[cur ^ 1], ctrl, n);
             aesc_hook<<<kCols, 128, 0, s>>>(st->col_src.as<uint32_t>(), csr, adj, tsl, P[cur ^ 1], ctrl,
                                             g_hat_dev);
         };
