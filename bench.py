@@ -338,15 +338,9 @@ def aesc_cfg3_summary(sb, args):
            "walk_steps_per_s": est.total_walk_steps / wall, "lambda_hat": est.plan.lambda_hat,
            "tau": int(est.plan.max_tau)}
     if not args.no_cpu_baseline:
-        from oracle.oracle import Reference, reference_available
-        if reference_available():
-            R = Reference()
-            r = R.aesc(R.from_csr(g.offsets, g.adjacency), epsilon=eps, delta=delta,
-                       sources=subset_sources(sb, g.n, cpu_sources))
-            res["cpu_baseline"] = {"value": r.plan_seconds + r.seconds * g.n / cpu_sources, "unit": "s",
-                                   "cores": R.max_threads(), "kind": "reference",
-                                   "sample": f"oracle/_ref aesc_source on {cpu_sources} sources, "
-                                             f"extrapolated x{g.n / cpu_sources:.1f}"}
+        cpu = aesc_cpu_reference(sb, g, eps, delta, cpu_sources)
+        if cpu is not None:
+            res["cpu_baseline"] = cpu
     return res
 
 
@@ -369,6 +363,46 @@ def subset_sources(sb, n, count):
     """First `count` vertices of a fixed counter_hash permutation."""
     keys = sb.counter_hash(SUBSET_TAG, np.arange(n, dtype=np.uint64))
     return np.argsort(keys, kind="stable")[:count].astype(np.uint32)
+
+
+def aesc_cpu_reference(sb, g, eps, delta, cpu_sources):
+    """oracle/_ref (the reference's aesc_source, OpenMP on every host core)
+    over the first `cpu_sources` sources of the subset permutation,
+    extrapolated like the GPU arm; None when oracle/_ref is not built."""
+    from oracle.oracle import Reference, reference_available
+    if not reference_available():
+        return None
+    R = Reference()
+    rg = R.from_csr(g.offsets, g.adjacency)
+    cs = subset_sources(sb, g.n, cpu_sources)
+    r = R.aesc(rg, epsilon=eps, delta=delta, sources=cs)
+    return {"value": (r.seconds * g.n / cpu_sources + r.plan_seconds), "unit": "s",
+            "cores": R.max_threads(), "kind": "reference",
+            "sample": f"oracle/_ref aesc_source over {cpu_sources} sources of the same "
+                      f"permutation ({r.seconds:.2f} s + plan {r.plan_seconds:.2f} s), "
+                      f"extrapolated x{g.n / cpu_sources:.1f}"}
+
+
+def run_aesc_reference(args):
+    """--impl reference for the AESC workloads: the reference's CPU path on
+    this box's host cores (rank 0 only), same metric and extrapolation."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import paper_2410_14056_b200 as sb  # graph generators only (host code)
+    spec, eps, delta, _, cpu_sources = AESC_WORKLOADS[args.workload]
+    g = make_aesc_graph(sb, spec)
+    cpu = aesc_cpu_reference(sb, g, eps, delta, cpu_sources)
+    if cpu is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref was not built"}))
+        return
+    print(json.dumps({
+        "impl": "reference", "metric": "TGT+ all-edges SC wall time", "value": cpu["value"],
+        "unit": "s", "n_gpus": world, "steps": 1, "warmup": 0, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {spec} n={g.n} m={g.m} eps={eps} delta={delta}"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": cpu["value"], "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
 def run_aesc_bench(args):
@@ -447,17 +481,7 @@ def run_aesc_bench(args):
         achieved = walk_rate * 96 / 1e9  # 96 B/step per lane
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            from oracle.oracle import Reference, reference_available
-            if reference_available():
-                R = Reference()
-                rg = R.from_csr(g.offsets, g.adjacency)
-                cs = subset_sources(sb, g.n, cpu_sources)
-                r = R.aesc(rg, epsilon=eps, delta=delta, sources=cs)
-                cpu = {"value": (r.seconds * g.n / cpu_sources + r.plan_seconds), "unit": "s",
-                       "cores": R.max_threads(), "kind": "reference",
-                       "sample": f"oracle/_ref aesc_source over {cpu_sources} sources of the same "
-                                 f"permutation ({r.seconds:.2f} s + plan {r.plan_seconds:.2f} s), "
-                                 f"extrapolated x{g.n / cpu_sources:.1f}"}
+            cpu = aesc_cpu_reference(sb, g, eps, delta, cpu_sources)
         out = {
             "metric": "TGT+ all-edges SC wall time", "value": full_estimate, "unit": "s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -478,7 +502,9 @@ def run_aesc_bench(args):
                          "bytes_per_step": 96, "peak_source": peak_src,
                          "note": "per-lane accounting; SABA-sorted warps share most gathers, so frac can exceed 1"},
             "cpu_baseline": cpu,
-            "e2e": {"value": plan_s + (e2e_t.item() / args.steps - plan_s) * scale, "unit": "s",
+            # the e2e-only work (pinned CSR upload, device replica build) is a
+            # per-run cost: added once, not multiplied by the extrapolation
+            "e2e": {"value": full_estimate + max(0.0, e2e_t.item() / args.steps - measured), "unit": "s",
                     "h2d_bytes_per_step": int(g.offsets.nbytes + g.adjacency.nbytes),
                     "d2h_bytes_per_step": int(est.g_hat.nbytes)},
             "gpu_launches": int(est.launches) * args.steps,
@@ -492,7 +518,8 @@ def run_aesc_bench(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 20 for walk campaigns, 2 for AESC workloads)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="saba", choices=["saba", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS) + sorted(AESC_WORKLOADS))
@@ -501,10 +528,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-aesc", action="store_true", help="skip the cfg3 AESC summary of the default run")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 2 if args.workload in AESC_WORKLOADS else 20
     if args.workload in AESC_WORKLOADS:
         if args.impl == "reference":
-            print(json.dumps({"impl": "reference", "unavailable":
-                              "AESC reference arm: see the cpu_baseline field of the saba arm"}))
+            run_aesc_reference(args)
             return
         run_aesc_bench(args)
     elif args.impl == "reference":

@@ -986,6 +986,18 @@ void validate_cfg(const saba_cu_aesc_config& c) {
 }
 
 // Host plan of one walk phase: slots -> groups -> chunks, tiles in pair order.
+int bits_for(uint32_t x) {
+    int b = 0;
+    while ((1ull << b) < x) ++b;
+    return b;
+}
+
+// Seed bits of the walk-sort key for a chunk whose largest bouquet has
+// max_pairs walks: about 32 walks per bucket, in [4, kSeedBits].
+uint32_t seed_bits(uint32_t max_pairs) {
+    return uint32_t(std::min<int>(kSeedBits, std::max(4, bits_for(max_pairs / 32) + 1)));
+}
+
 struct TileBuilder {
     struct Chunk {
         std::vector<WalkGroup> groups;
@@ -1012,9 +1024,16 @@ struct TileBuilder {
         const double inv_n = 1.0 / double(n_req);
         for (uint64_t k0 = 0; k0 < n_req; k0 += kGroupPairs) {
             const uint32_t pairs = uint32_t(std::min<uint64_t>(kGroupPairs, n_req - k0));
-            if (chunks.empty() || chunks.back().walks + 2ull * pairs > kChunkWalks ||
-                chunks.back().groups.size() >= (1u << (31 - kSeedBits)))
-                chunks.emplace_back();
+            bool close = chunks.empty() || chunks.back().walks + 2ull * pairs > kChunkWalks ||
+                         chunks.back().groups.size() >= (1u << (31 - kSeedBits));
+            if (!close && chunks.back().walks >= (1u << 22)) {
+                // keep the (group, side, seed) key within 24 bits: 3 radix passes
+                const Chunk& c = chunks.back();
+                const int key_bits = int(seed_bits(std::max(c.max_pairs, pairs))) + 1 +
+                                     bits_for(uint32_t(c.groups.size()) + 1);
+                close = key_bits > 24;
+            }
+            if (close) chunks.emplace_back();
             Chunk& c = chunks.back();
             const uint32_t gi = uint32_t(c.groups.size());
             c.groups.push_back({edge_seed, k0, pairs, c.walks, vi, vj, len, col});
@@ -1030,11 +1049,6 @@ struct TileBuilder {
     }
 };
 
-int bits_for(uint32_t x) {
-    int b = 0;
-    while ((1ull << b) < x) ++b;
-    return b;
-}
 
 // Walk phase: per chunk keygen -> radix sort (group, seed top bits) -> sorted
 // walks -> pair tiles; then the per-slot fold into g_hat.
@@ -1080,7 +1094,7 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         if (merge)
             for (uint32_t cp : c.col_pairs) max_seg = std::max(max_seg, cp);
         uint32_t* gid = merge ? static_cast<uint32_t*>(st->gid.ensure(sizeof(uint32_t) * nw)) : nullptr;
-        const uint32_t sb = uint32_t(std::min<int>(kSeedBits, std::max(4, bits_for(max_seg / 32) + 1)));
+        const uint32_t sb = seed_bits(max_seg);
         aesc_keygen<<<g->sm_count * 8, 256, 0, s>>>(dg, doff, ng, nw, sb, keys.Current(), vals.Current(), gid);
         SABA_CUDA_CHECK(cudaGetLastError());
         const int end_bit = merge ? int(sb) + std::max(1, bits_for(kCols + ng))
