@@ -84,6 +84,14 @@ struct AescState {
 
 constexpr int kWorkspaces = 2;  // batches in flight (one host thread + stream each)
 
+// tau of a directed slot on the host: one value for a uniform plan, else a
+// caller-owned per-slot array
+struct SlotTau {
+    const uint32_t* v = nullptr;
+    uint32_t uni = 0;
+    uint32_t operator[](uint64_t slot) const { return v ? v[slot] : uni; }
+};
+
 void release_aesc_state(saba_cu_graph* g) {
     delete[] g->aesc;
     g->aesc = nullptr;
@@ -750,7 +758,7 @@ struct Engine {
     AescState* st;
     cudaStream_t s;
     AescParams p{};
-    std::vector<uint32_t> tau_slot;  // host copy, per directed slot
+    SlotTau tau_slot;  // tau per directed slot (host side)
     uint32_t launches = 0;
     uint64_t pairs = 0, steps = 0;
     cudaGraphExec_t depth_graph = nullptr;  // kDepthsPerGraph captured depths
@@ -832,10 +840,15 @@ struct Engine {
         st->heavy_built = true;
     }
 
-    void upload_tau(std::vector<uint32_t> ts) {
-        tau_slot = std::move(ts);
-        SABA_CUDA_CHECK(cudaMemcpyAsync(buf<uint32_t>(st->tau_slot, tau_slot.size()), tau_slot.data(),
-                                        sizeof(uint32_t) * tau_slot.size(), cudaMemcpyHostToDevice, s));
+    // a per-slot array must outlive the engine; a uniform plan is filled on the device
+    void upload_tau(const SlotTau& t) {
+        tau_slot = t;
+        const size_t slots = 2 * g->m;
+        uint32_t* d = buf<uint32_t>(st->tau_slot, slots);
+        if (t.v == nullptr)
+            fill_u32(d, t.uni, slots, s);
+        else
+            copy_h2d(d, t.v, sizeof(uint32_t) * slots, s);
     }
 
     uint32_t deg(uint32_t v) const { return g->h_off[v + 1] - g->h_off[v]; }
@@ -1148,6 +1161,45 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
     SABA_CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
+// Power-iteration SpMV of the truncation plan (aesc.hpp:160-170) on the
+// device, rounding exactly like the host loop: y[u] = (sum in slot order of
+// x[a] * isd[a]) * isd[u], one multiply then one add per neighbour. The
+// sequential reductions stay on the host, so lambda_hat is bit-identical.
+__global__ void plan_spmv_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                                 const double* __restrict__ x, const double* __restrict__ isd,
+                                 double* __restrict__ y, uint32_t n) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        const uint2 r = csr[u];
+        double acc = 0.0;
+        for (uint32_t s = r.x; s < r.x + r.y; ++s) {
+            const uint32_t a = adj[s];
+            acc = __dadd_rn(acc, __dmul_rn(x[a], isd[a]));
+        }
+        y[u] = __dmul_rn(acc, isd[u]);
+    }
+}
+
+struct DeviceSpmv {
+    saba_cu_graph* g;
+    DevBuf x, isd, y;
+    bool isd_up = false;
+    SpmvFn fn() {
+        return [this](const std::vector<double>& hx, const std::vector<double>& hisd, std::vector<double>& hy) {
+            const uint32_t n = g->n;
+            const size_t bytes = sizeof(double) * n;
+            if (!isd_up) {
+                copy_h2d(isd.ensure(bytes), hisd.data(), bytes, 0);
+                isd_up = true;
+            }
+            copy_h2d(x.ensure(bytes), hx.data(), bytes, 0);
+            plan_spmv_kernel<<<(n + 255) / 256, 256>>>(g->d_csr, g->d_adj, x.as<double>(), isd.as<double>(),
+                                                       static_cast<double*>(y.ensure(bytes)), n);
+            SABA_CUDA_CHECK(cudaGetLastError());
+            copy_d2h(hy.data(), y.p, bytes, 0);
+        };
+    }
+};
+
 AescParams make_params(const saba_cu_graph* g, double eps, double delta, int64_t cap) {
     AescParams p{};
     p.eps = eps;
@@ -1171,9 +1223,12 @@ int saba_cu_truncated_lengths(saba_cu_graph* g, double epsilon, uint32_t power_i
                               double* lambda_hat, int* clamped) {
     return guard([&] {
         check_arg(g && tau_out && lambda_hat && clamped, "null argument");
+        DeviceScope scope(g->device);
         const HostCsr h{g->n, g->m, g->h_off.data(), host_adj(g).data()};
+        DeviceSpmv dev{g};
+        const SpmvFn spmv = dev.fn();
         const Plan p = host_truncated_lengths(h, slot_edges(g), epsilon, power_iterations,
-                                              max_truncation, per_edge != 0);
+                                              max_truncation, per_edge != 0, &spmv);
         std::copy(p.tau.begin(), p.tau.end(), tau_out);
         *lambda_hat = p.lambda_hat;
         *clamped = p.clamped ? 1 : 0;
@@ -1189,28 +1244,52 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
         validate_cfg(*cfg);
         check_arg(shard_count >= 1 && shard_index < shard_count, "bad shard index/count");
         DeviceScope scope(g->device);
+        const bool trace = getenv("SABA_TRACE") != nullptr;
+        auto T = std::chrono::steady_clock::now();
+        auto lap = [&](const char* what) {
+            if (!trace) return;
+            const auto T1 = std::chrono::steady_clock::now();
+            fprintf(stderr, "[saba] aesc %-26s %9.2f ms\n", what,
+                    std::chrono::duration<double, std::milli>(T1 - T).count());
+            T = T1;
+        };
         const auto t_plan0 = std::chrono::steady_clock::now();
         const auto& hadj = host_adj(g);
+        lap("host adjacency");
         const HostCsr h{g->n, g->m, g->h_off.data(), hadj.data()};
         check_data(host_is_connected(h), "aesc: spanning centrality requires a connected graph");
+        lap("connectivity");
         const auto& se = slot_edges(g);
+        lap("slot edges");
         // aesc.hpp:649: the plan is built for epsilon / 2
+        DeviceSpmv dev{g};
+        const SpmvFn spmv = dev.fn();
         const Plan plan = host_truncated_lengths(h, se, cfg->epsilon / 2.0, cfg->power_iterations,
-                                                 cfg->max_truncation, cfg->per_edge_tau != 0);
+                                                 cfg->max_truncation, cfg->per_edge_tau != 0, &spmv);
         const auto t_plan1 = std::chrono::steady_clock::now();
+        lap("truncation plan");
         const uint32_t n = g->n;
         const uint64_t m = g->m;
         for (uint64_t i = 0; i < source_count; ++i) check_arg(sources[i] < n, "source out of range");
         if (fat_fits_l2(g) && aesc_fat_enabled()) ensure_fat(g);  // before the workers start
-
+        lap("fat adjacency");
         Engine E(g);
+        lap("engine");
         E.p = make_params(g, cfg->epsilon, cfg->delta, cfg->switch_depth_cap);
         E.p.bip_init = plan.bipartite ? 1.0 / (2.0 * double(m)) : 0.0;  // aesc.hpp:657
         E.p.uniform_tau = plan.uniform ? 1 : 0;
         E.p.tau_uniform = plan.tau.empty() ? 0 : plan.tau[0];
-        std::vector<uint32_t> ts(2 * m);
-        for (uint64_t s = 0; s < 2 * m; ++s) ts[s] = plan.tau[se[s]];
+        // tau per directed slot: a constant for a uniform plan (the default)
+        std::vector<uint32_t> ts_v;
+        SlotTau ts{nullptr, plan.tau.empty() ? 0u : plan.tau[0]};
+        if (!plan.uniform) {
+            ts_v.resize(2 * m);
+#pragma omp parallel for schedule(static)
+            for (int64_t s = 0; s < int64_t(2 * m); ++s) ts_v[s] = plan.tau[se[s]];
+            ts.v = ts_v.data();
+        }
         E.upload_tau(ts);
+        lap("tau per slot");
         double* d_g = static_cast<double*>(E.st->g_hat.ensure(sizeof(double) * 2 * m));
         SABA_CUDA_CHECK(cudaMemsetAsync(d_g, 0, sizeof(double) * 2 * m, E.s));
 
@@ -1242,6 +1321,7 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
             engines.back()->upload_tau(ts);
         }
         SABA_CUDA_CHECK(cudaStreamSynchronize(engines[0]->s));  // g_hat zeroed before any batch
+        lap("workers ready");
         std::vector<float> prop_ms(kWorkspaces, 0.f), walk_ms(kWorkspaces, 0.f);
         std::vector<std::exception_ptr> failure(kWorkspaces);
         const auto t0 = std::chrono::steady_clock::now();
@@ -1257,9 +1337,11 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
                 for (size_t b0 = size_t(w) * kCols; b0 < list.size(); b0 += size_t(nworkers) * kCols) {
                     const std::vector<uint32_t> cols(list.begin() + b0,
                                                      list.begin() + std::min(list.size(), b0 + kCols));
+                    const auto h0 = std::chrono::steady_clock::now();
                     SABA_CUDA_CHECK(cudaEventRecord(e0, W.s));
                     const std::vector<uint32_t> tt = W.propagate(cols, d_g);
                     SABA_CUDA_CHECK(cudaEventRecord(e1, W.s));
+                    const auto h1 = std::chrono::steady_clock::now();
                     tb.clear();
                     for (size_t c = 0; c < cols.size(); ++c) {
                         const uint32_t src = cols[c];
@@ -1292,10 +1374,12 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
                     // when the batch's union frontier went dense
                     const uint32_t tt_max = *std::max_element(tt.begin(), tt.end());
                     const bool use_bits = bitmap_mode == 1 || (bitmap_mode == 2 && tt_max <= 4);
+                    const auto h2 = std::chrono::steady_clock::now();
                     run_tiles(g, W.st, W.s, tb, W.st->R.as<double>(),
                               use_bits ? W.st->bits.as<uint32_t>() : nullptr, cfg->hash_multiplier,
                               d_g, &W.launches);
                     SABA_CUDA_CHECK(cudaEventRecord(e2, W.s));
+                    const auto h3 = std::chrono::steady_clock::now();
                     W.clear_batch(int(cols.size()));
                     SABA_CUDA_CHECK(cudaEventSynchronize(e2));
                     float ta = 0.f, tw = 0.f;
@@ -1303,6 +1387,13 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
                     SABA_CUDA_CHECK(cudaEventElapsedTime(&tw, e1, e2));
                     prop_ms[w] += ta;
                     walk_ms[w] += tw;
+                    if (trace) {
+                        const auto h4 = std::chrono::steady_clock::now();
+                        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+                        fprintf(stderr, "[saba] aesc w%d batch %zu: propagate %.2f ms (device %.2f), tiles %.2f, "
+                                "run_tiles %.2f (device walk %.2f), clear+sync %.2f\n", w, b0 / kCols, ms(h0, h1), ta,
+                                ms(h1, h2), ms(h2, h3), tw, ms(h3, h4));
+                    }
                 }
                 SABA_CUDA_CHECK(cudaStreamSynchronize(W.s));
                 cudaEventDestroy(e0);
@@ -1318,6 +1409,7 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
         for (auto& t : threads) t.join();
         for (auto& f : failure)
             if (f) std::rethrow_exception(f);
+        lap("batches");
         Engine& E0 = *engines[0];
         for (int w = 1; w < nworkers; ++w) {
             E0.pairs += engines[w]->pairs;
@@ -1334,10 +1426,10 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
             aesc_symmetrise<<<g->sm_count * 4, 256, 0, E0.s>>>(g->d_csr, g->d_adj, d_se, n, d_g, d_s);
             SABA_CUDA_CHECK(cudaGetLastError());
             ++E0.launches;
-            SABA_CUDA_CHECK(cudaMemcpyAsync(s_hat_out, d_s, sizeof(double) * m, cudaMemcpyDeviceToHost, E0.s));
+            copy_d2h(s_hat_out, d_s, sizeof(double) * m, E0.s);
         }
-        SABA_CUDA_CHECK(cudaMemcpyAsync(g_hat_out, d_g, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost, E0.s));
-        SABA_CUDA_CHECK(cudaStreamSynchronize(E0.s));
+        copy_d2h(g_hat_out, d_g, sizeof(double) * 2 * m, E0.s);
+        lap("g_hat to host");
         const auto t1 = std::chrono::steady_clock::now();
         std::copy(plan.tau.begin(), plan.tau.end(), tau_out);
         std::copy(tt_all.begin(), tt_all.end(), tau_tilde_out);
@@ -1372,9 +1464,10 @@ int saba_cu_propagate(saba_cu_graph* g, uint32_t source, const uint32_t* tau, do
         Engine E(g);
         E.p = make_params(g, epsilon, delta, cap);
         E.p.uniform_tau = 0;  // caller-supplied tau: exact budget loop
-        std::vector<uint32_t> ts(2 * g->m);
-        for (uint64_t s = 0; s < 2 * g->m; ++s) ts[s] = tau[se[s]];
-        E.upload_tau(std::move(ts));
+        std::vector<uint32_t> ts_v(2 * g->m);
+#pragma omp parallel for schedule(static)
+        for (int64_t s = 0; s < int64_t(2 * g->m); ++s) ts_v[s] = tau[se[s]];
+        E.upload_tau(SlotTau{ts_v.data(), 0});
         double* d_g = static_cast<double*>(E.st->g_hat.ensure(sizeof(double) * std::max<uint64_t>(2 * g->m, 1)));
         const std::vector<uint32_t> tt = E.propagate({source}, d_g);
         // column 0 of P at the switch depth: depth d always lives in P[d & 1]

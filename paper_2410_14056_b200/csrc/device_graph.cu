@@ -1,5 +1,7 @@
 // K0: device CSR upload and the handle lifecycle; library identification.
 #include <chrono>
+#include <mutex>
+#include <omp.h>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -92,6 +94,111 @@ void* pool_alloc(size_t bytes) {
     SABA_CUDA_CHECK(cudaMallocAsync(&p, bytes, 0));
     SABA_CUDA_CHECK(cudaStreamSynchronize(0));
     return p;
+}
+
+namespace {
+constexpr size_t kStageBytes = size_t(32) << 20;  // per staging buffer
+struct Staging {
+    std::mutex mu;
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int device = -1;
+    void ensure(int dev) {
+        if (buf[0] && device == dev) return;
+        for (int i = 0; i < 2; ++i) {
+            if (!buf[i]) SABA_CUDA_CHECK(cudaMallocHost(&buf[i], kStageBytes));
+            if (ev[i]) cudaEventDestroy(ev[i]);
+            SABA_CUDA_CHECK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        }
+        device = dev;
+    }
+};
+Staging g_staging;
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    constexpr size_t kPiece = size_t(1) << 20;
+    const int64_t pieces = int64_t((bytes + kPiece - 1) / kPiece);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < pieces; ++i) {
+        const size_t o = size_t(i) * kPiece;
+        std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                    std::min(kPiece, bytes - o));
+    }
+}
+
+__global__ void fill_u32_kernel(uint32_t* __restrict__ d, uint32_t v, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        d[i] = v;
+}
+}  // namespace
+
+void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return;
+    if (bytes <= (size_t(4) << 20) || is_pinned(src)) {
+        SABA_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        SABA_CUDA_CHECK(cudaStreamSynchronize(s));
+        return;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_staging.mu);
+    g_staging.ensure(dev);
+    size_t i = 0;
+    for (size_t o = 0; o < bytes; o += kStageBytes, ++i) {
+        const int b = int(i & 1);
+        const size_t len = std::min(kStageBytes, bytes - o);
+        if (i >= 2) SABA_CUDA_CHECK(cudaEventSynchronize(g_staging.ev[b]));  // buffer free again
+        par_memcpy(g_staging.buf[b], static_cast<const char*>(src) + o, len);
+        SABA_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(dst) + o, g_staging.buf[b], len,
+                                        cudaMemcpyHostToDevice, s));
+        SABA_CUDA_CHECK(cudaEventRecord(g_staging.ev[b], s));
+    }
+    SABA_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return;
+    if (bytes <= (size_t(4) << 20) || is_pinned(dst)) {
+        SABA_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        SABA_CUDA_CHECK(cudaStreamSynchronize(s));
+        return;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_staging.mu);
+    g_staging.ensure(dev);
+    const size_t chunks = (bytes + kStageBytes - 1) / kStageBytes;
+    auto issue = [&](size_t i) {
+        const int b = int(i & 1);
+        const size_t o = i * kStageBytes, len = std::min(kStageBytes, bytes - o);
+        SABA_CUDA_CHECK(cudaMemcpyAsync(g_staging.buf[b], static_cast<const char*>(src) + o, len,
+                                        cudaMemcpyDeviceToHost, s));
+        SABA_CUDA_CHECK(cudaEventRecord(g_staging.ev[b], s));
+    };
+    issue(0);
+    if (chunks > 1) issue(1);
+    for (size_t i = 0; i < chunks; ++i) {
+        const int b = int(i & 1);
+        const size_t o = i * kStageBytes, len = std::min(kStageBytes, bytes - o);
+        SABA_CUDA_CHECK(cudaEventSynchronize(g_staging.ev[b]));
+        par_memcpy(static_cast<char*>(dst) + o, g_staging.buf[b], len);
+        if (i + 2 < chunks) issue(i + 2);
+    }
+}
+
+void fill_u32(uint32_t* dst, uint32_t value, size_t count, cudaStream_t s) {
+    if (count == 0) return;
+    fill_u32_kernel<<<1184, 256, 0, s>>>(dst, value, count);
+    SABA_CUDA_CHECK(cudaGetLastError());
 }
 
 void pool_free(void* p) {

@@ -109,4 +109,12 @@ bool ensure_fat(saba_cu_graph* g);
 inline bool fat_fits_l2(const saba_cu_graph* g) { return 16 * g->m <= (uint64_t(48) << 20); }
 constexpr uint32_t kPackBits = 21;
 constexpr uint32_t kPackMax = 1u << kPackBits;  // ids must be < 2^21 to pack
+
+// Host <-> device copies of large caller-owned (pageable) buffers at PCIe
+// speed: through a pinned double-buffered staging ring with a parallel host
+// memcpy; already-pinned buffers go direct. Both return when the copy is
+// complete (the caller's buffer may be reused).
+void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
+void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
+void fill_u32(uint32_t* dst, uint32_t value, size_t count, cudaStream_t s);
 }

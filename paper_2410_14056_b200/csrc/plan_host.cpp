@@ -103,7 +103,8 @@ bool host_bipartition(const HostCsr& g, std::vector<char>& side) {
     return true;
 }
 
-double host_estimate_decay(const HostCsr& g, uint32_t iters, bool bip, const std::vector<char>& side) {
+double host_estimate_decay(const HostCsr& g, uint32_t iters, bool bip, const std::vector<char>& side,
+                           const SpmvFn* spmv) {
     const uint32_t n = g.n;
     const double two_m = 2.0 * double(g.m);
     std::vector<double> phi(n), isd(n), x(n), y(n), z(n), sgn(n, 1.0);
@@ -141,13 +142,17 @@ double host_estimate_decay(const HostCsr& g, uint32_t iters, bool bip, const std
     // the norm) stay sequential, so lambda_hat is bit-identical.
     const int64_t N = n;
     for (uint32_t it = 0; it < iters; ++it) {
+        if (spmv) {
+            (*spmv)(x, isd, y);
+        } else {
 #pragma omp parallel for schedule(static)
-        for (int64_t v = 0; v < N; ++v) z[v] = x[v] * isd[v];
+            for (int64_t v = 0; v < N; ++v) z[v] = x[v] * isd[v];
 #pragma omp parallel for schedule(dynamic, 1024)
-        for (int64_t u = 0; u < N; ++u) {
-            double acc = 0.0;
-            for (uint32_t s = g.off[u]; s < g.off[u + 1]; ++s) acc += z[g.adj[s]];
-            y[u] = acc * isd[u];
+            for (int64_t u = 0; u < N; ++u) {
+                double acc = 0.0;
+                for (uint32_t s = g.off[u]; s < g.off[u + 1]; ++s) acc += z[g.adj[s]];
+                y[u] = acc * isd[u];
+            }
         }
         project(y);
         const double ny = norm(y);
@@ -174,7 +179,7 @@ uint32_t make_odd_clamped(double raw, uint32_t max_truncation, bool& clamped) {
 }  // namespace
 
 Plan host_truncated_lengths(const HostCsr& g, const std::vector<uint32_t>& slot_edge, double eps,
-                            uint32_t omega, uint32_t max_truncation, bool per_edge) {
+                            uint32_t omega, uint32_t max_truncation, bool per_edge, const SpmvFn* spmv) {
     check_arg(eps > 0.0 && eps < 1.0, "truncated_lengths: epsilon must be in (0,1)");
     check_arg(omega >= 1, "truncated_lengths: omega must be >= 1");
     check_arg(max_truncation >= 1, "truncated_lengths: tau_max must be >= 1");
@@ -185,7 +190,7 @@ Plan host_truncated_lengths(const HostCsr& g, const std::vector<uint32_t>& slot_
     const bool bip = bipartition_connected(g, parity, side);
     Plan p;
     p.bipartite = bip;
-    p.lambda_hat = host_estimate_decay(g, omega, bip, side);
+    p.lambda_hat = host_estimate_decay(g, omega, bip, side, spmv);
     auto tau_for = [&](double dmax) -> uint32_t {
         if (p.lambda_hat >= 1.0 - 1e-6) {
             p.clamped = true;
