@@ -41,9 +41,12 @@ MASTER_SEED = 42
 GRAPH_SEED = 1
 
 
-def make_graph(sb, spec):
+def make_graph(sb, spec, device=None):
+    """device: build on that GPU (csrc/graph_build.cu, bit-identical CSR;
+    tests/test_graph_build_gpu.py); None = host builder (the reference arm)."""
     if spec[0] == "rmat":
-        return sb.make_rmat(spec[1], spec[2], 0.57, 0.19, 0.19, seed=GRAPH_SEED, keep_lcc=True)
+        return sb.make_rmat(spec[1], spec[2], 0.57, 0.19, 0.19, seed=GRAPH_SEED, keep_lcc=True,
+                            device=device)
     return sb.make_erdos_renyi(spec[1], spec[2], GRAPH_SEED)
 
 
@@ -200,7 +203,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     spec, walks, L = WORKLOADS[args.workload]
     mode = sb.WalkMode.Saba if args.mode == "saba" else sb.WalkMode.Hash
-    g = make_graph(sb, spec)
+    g = make_graph(sb, spec, device=local)
     cfg = sb.CampaignConfig(length=L, master_seed=MASTER_SEED, mode=mode)
     total_walks = walks * world
     steps_per_rank = walks * (L - 1)
@@ -353,10 +356,12 @@ AESC_WORKLOADS = {
 SUBSET_TAG = 0x5355425345  # "SUBSE": fixed source permutation of the subset protocol
 
 
-def make_aesc_graph(sb, spec):
+def make_aesc_graph(sb, spec, device=None):
     if spec[0] == "rmat":
-        return sb.make_rmat(spec[1], spec[2], 0.57, 0.19, 0.19, seed=GRAPH_SEED, keep_lcc=True)
-    return sb.make_chung_lu(spec[1], 2.2, 78.0, 30000.0, seed=GRAPH_SEED, keep_lcc=True)
+        return sb.make_rmat(spec[1], spec[2], 0.57, 0.19, 0.19, seed=GRAPH_SEED, keep_lcc=True,
+                            device=device)
+    return sb.make_chung_lu(spec[1], 2.2, 78.0, 30000.0, seed=GRAPH_SEED, keep_lcc=True,
+                            device=device)
 
 
 def subset_sources(sb, n, count):
@@ -419,7 +424,7 @@ def run_aesc_bench(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     spec, eps, delta, per_gpu, cpu_sources = AESC_WORKLOADS[args.workload]
-    g = make_aesc_graph(sb, spec)
+    g = make_aesc_graph(sb, spec, device=local)
     cfg = sb.AescConfig(epsilon=eps, delta=delta)
     if per_gpu:
         sources = subset_sources(sb, g.n, per_gpu * world)

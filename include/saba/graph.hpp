@@ -62,8 +62,11 @@ public:
     [[nodiscard]] uint32_t max_degree() const noexcept { return max_degree_; }
 
     /// Canonicalising constructor: loops dropped, duplicates / reversals
-    /// merged, n = max(n_hint, largest id + 1).
-    static Graph from_edges(uint32_t n_hint, std::vector<std::pair<uint32_t, uint32_t>> pairs) {
+    /// merged, n = max(n_hint, largest id + 1). `device` >= 0 (an extension;
+    /// default host, as the reference) runs the canonicalisation on that GPU
+    /// (saba_cu_graph_from_edges): the same CSR, built by a device sort.
+    static Graph from_edges(uint32_t n_hint, std::vector<std::pair<uint32_t, uint32_t>> pairs,
+                            int device = -1) {
         std::vector<uint32_t> flat;
         flat.reserve(2 * pairs.size());
         for (const auto& [a, b] : pairs) {
@@ -71,7 +74,11 @@ public:
             flat.push_back(b);
         }
         saba_hgraph* h = nullptr;
-        detail::raise_on(saba_hgraph_from_edges(n_hint, flat.data(), pairs.size(), &h), "from_edges");
+        if (device >= 0)
+            detail::raise_on(saba_cu_graph_from_edges(n_hint, flat.data(), pairs.size(), 0, device, &h),
+                             "from_edges");
+        else
+            detail::raise_on(saba_hgraph_from_edges(n_hint, flat.data(), pairs.size(), &h), "from_edges");
         Graph g;
         g.adopt(h);
         return g;

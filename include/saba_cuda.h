@@ -83,6 +83,17 @@ SABA_API int saba_gen_chung_lu(uint32_t n, double gamma, double mean_degree, dou
 SABA_API int saba_gen_scale_free(uint32_t n, uint32_t attach, uint64_t seed, saba_hgraph** out);
 SABA_API int saba_gen_random_connected(uint32_t n, uint32_t extra, uint64_t seed, saba_hgraph** out);
 SABA_API int saba_hgraph_largest_component(const saba_hgraph* in, saba_hgraph** out);
+/* The same constructions on a device, bit-identical CSR:
+ * Graph::from_edges (graph.hpp:86-105) as a device radix sort + unique of the
+ * directed pairs, optionally reduced to the largest connected component
+ * (device union-find); the R-MAT / Chung–Lu samplers above with their edge
+ * samples drawn on the device. */
+SABA_API int saba_cu_graph_from_edges(uint32_t n_hint, const uint32_t* pairs, uint64_t count, int keep_lcc,
+                                      int device, saba_hgraph** out);
+SABA_API int saba_cu_gen_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                              uint64_t seed, int keep_lcc, int device, saba_hgraph** out);
+SABA_API int saba_cu_gen_chung_lu(uint32_t n, double gamma, double mean_degree, double max_degree,
+                                  uint64_t seed, int keep_lcc, int device, saba_hgraph** out);
 SABA_API uint32_t saba_hgraph_vertex_count(const saba_hgraph* g);
 SABA_API uint64_t saba_hgraph_edge_count(const saba_hgraph* g);
 /* copy out offsets[n+1] and adjacency[2m] */

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsaba_cuda.so")
+# SABA_LIB points at an experiment build of the same library (tools/build_variant.sh)
+LIB_PATH = os.environ.get("SABA_LIB") or os.path.join(HERE, "libsaba_cuda.so")
 
 SABA_OK, SABA_EINVAL, SABA_EDATA, SABA_ECUDA = 0, 1, 2, 3
 
@@ -74,6 +75,11 @@ SIGNATURES = {
     "saba_gen_scale_free": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint64, vpp]),
     "saba_gen_random_connected": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint64, vpp]),
     "saba_hgraph_largest_component": (C.c_int, [vp, vpp]),
+    "saba_cu_graph_from_edges": (C.c_int, [C.c_uint32, u32p, C.c_uint64, C.c_int, C.c_int, vpp]),
+    "saba_cu_gen_rmat": (C.c_int, [C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double,
+                                   C.c_uint64, C.c_int, C.c_int, vpp]),
+    "saba_cu_gen_chung_lu": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                       C.c_int, C.c_int, vpp]),
     "saba_hgraph_vertex_count": (C.c_uint32, [vp]),
     "saba_hgraph_edge_count": (C.c_uint64, [vp]),
     "saba_hgraph_csr": (C.c_int, [vp, u32p, u32p]),

@@ -38,9 +38,9 @@
 // Buffer invariant: outside the rows a batch touches, P/Q/M/R are all zero.
 // Double buffering keeps it within a batch (support(l+2) contains
 // support(l)), and aesc_clear restores it between batches.
-#include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_reduce.cuh>
-#include <cub/device/device_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -68,7 +68,8 @@ struct AescState {
     DevBuf ulist[2], ucount, flag, tflag, tlist, tcount;
     DevBuf col_src, col_tau, degsum[2], tt, ctrl;  // per-column state
     DevBuf tau_slot, slot_edge_d, g_hat, s_hat, rho1;
-    DevBuf tiles, slots, partials, groups, woffs, keys[2], vals[2], score, sort_tmp, gid;
+    DevBuf tiles, slots, partials, groups, keys[2], vals[2], score, sort_tmp;
+    DevBuf sort_segs, cb_seg, cb_cnt, cb_start, cb_cursor, coarse_tiles;  // K4s walk bucketing
     DevBuf heavy_rows, piece_off, pieces, part, part_mask;  // hub-row split (static per graph)
     uint32_t nheavy = 0, npieces = 0;
     DevBuf light_order;  // light rows by descending degree (dense depths)
@@ -281,29 +282,37 @@ __global__ void aesc_expand(const uint2* __restrict__ csr, const uint32_t* __res
 // order: a deterministic function of the row alone, and no hub row sits on
 // one warp's critical path.
 constexpr uint32_t kHeavy = 256;
+#ifndef SABA_PULL_UNROLL
+#define SABA_PULL_UNROLL 6
+#endif
+constexpr int kPullUnroll = SABA_PULL_UNROLL;  // Q-row gathers in flight per warp
 
 // Sum of Q rows (2 columns per lane) and OR of support masks over the
-// neighbour slots [b, e), in slot order; 8 gathers in flight per warp.
+// neighbour slots [b, e), in slot order; kPullUnroll gathers in flight per warp.
 __device__ __forceinline__ void pull_range(const uint32_t* __restrict__ adj,
                                            const double* __restrict__ Qc,
                                            const unsigned long long* __restrict__ Mc, uint32_t b,
-                                           uint32_t e, uint32_t lane, double& a0, double& a1,
+                                           uint32_t e, uint32_t lane, bool need, double& a0, double& a1,
                                            unsigned long long& mask) {
+    // need = one of the lane's two columns is still active: lanes of frozen
+    // columns skip their half-sector of every Q row (their sums are zeroed
+    // by pull_store anyway), so late depths move fewer L2 sectors.
+    constexpr int U = kPullUnroll;
     for (uint32_t s0 = b; s0 < e; s0 += 32) {
         const uint32_t cnt = min(32u, e - s0);
         const uint32_t mine = lane < cnt ? adj[s0 + lane] : 0u;
         uint32_t k = 0;
-        for (; k + 8 <= cnt; k += 8) {
-            double2 q[8];
-            unsigned long long mm[8];
+        for (; k + U <= cnt; k += U) {
+            double2 q[U];
+            unsigned long long mm[U];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < U; ++j) {
                 const uint32_t v = __shfl_sync(0xffffffffu, mine, k + j);
                 mm[j] = Mc[v];
-                q[j] = reinterpret_cast<const double2*>(Qc + size_t(v) * kCols)[lane];
+                q[j] = need ? reinterpret_cast<const double2*>(Qc + size_t(v) * kCols)[lane] : make_double2(0.0, 0.0);
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < U; ++j) {
                 mask |= mm[j];
                 a0 += q[j].x;
                 a1 += q[j].y;
@@ -312,7 +321,8 @@ __device__ __forceinline__ void pull_range(const uint32_t* __restrict__ adj,
         for (; k < cnt; ++k) {
             const uint32_t v = __shfl_sync(0xffffffffu, mine, k);
             mask |= Mc[v];
-            const double2 q = reinterpret_cast<const double2*>(Qc + size_t(v) * kCols)[lane];
+            const double2 q = need ? reinterpret_cast<const double2*>(Qc + size_t(v) * kCols)[lane]
+                                   : make_double2(0.0, 0.0);
             a0 += q.x;
             a1 += q.y;
         }
@@ -356,7 +366,10 @@ struct HeavyPiece {
 
 // Pull SpMM over the candidate rows (sparse) or all rows (dense) with at
 // most kHeavy neighbours. Warp per row, lane = columns {2 lane, 2 lane + 1}.
-__global__ void __launch_bounds__(256)
+#ifndef SABA_PULL_MINB
+#define SABA_PULL_MINB 4  // 64 registers: 32 warps per SM keep more Q-row gathers in flight
+#endif
+__global__ void __launch_bounds__(256, SABA_PULL_MINB)
     aesc_pull(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
               const double* __restrict__ Qc, const unsigned long long* __restrict__ Mc,
               double* __restrict__ Pn, double* __restrict__ Qn, unsigned long long* __restrict__ Mn,
@@ -373,6 +386,7 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     const bool dense = ctrl[kDense] != 0;
     const uint32_t lane = threadIdx.x & 31;
+    const bool need = ((active >> (2 * lane)) & 3ull) != 0;
     unsigned long long ds0 = 0, ds1 = 0;
     if (dense && light_order) {
         // dense depths: hub-row pieces, then light rows in descending degree
@@ -387,7 +401,7 @@ __global__ void __launch_bounds__(256)
                 const HeavyPiece pc = pieces[i];
                 double a0 = 0.0, a1 = 0.0;
                 unsigned long long mask = 0;
-                pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, a0, a1, mask);
+                pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, need, a0, a1, mask);
                 reinterpret_cast<double2*>(part + size_t(i) * kCols)[lane] = make_double2(a0, a1);
                 if (lane == 0) part_mask[i] = mask;
                 continue;
@@ -396,7 +410,7 @@ __global__ void __launch_bounds__(256)
             const uint2 r = csr[x];
             double a0 = 0.0, a1 = 0.0;
             unsigned long long mask = 0;
-            pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, a0, a1, mask);
+            pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, need, a0, a1, mask);
             pull_store(x, r.y, a0, a1, mask, active, lane, Pn, Qn, Mn, ds0, ds1);
         }
         flush_degsum(bds, ds0, ds1, lane, degsum_next);
@@ -410,7 +424,7 @@ __global__ void __launch_bounds__(256)
         if (r.y > kHeavy) continue;  // pieces + combine
         double a0 = 0.0, a1 = 0.0;
         unsigned long long mask = 0;
-        pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, a0, a1, mask);
+        pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, need, a0, a1, mask);
         pull_store(x, r.y, a0, a1, mask, active, lane, Pn, Qn, Mn, ds0, ds1);
         if (lane == 0 && !dense) flag[x] = 0;
     }
@@ -427,17 +441,19 @@ __global__ void __launch_bounds__(256)
                      const unsigned long long* __restrict__ Mc, const uint32_t* __restrict__ flag,
                      double* __restrict__ part, unsigned long long* __restrict__ part_mask,
                      const unsigned long long* __restrict__ ctrl, uint32_t dynamic) {
-    if (!ctrl[kActive]) return;
+    const unsigned long long active = ctrl[kActive];
+    if (!active) return;
     const bool dense = ctrl[kDense] != 0;
     if (dense && dynamic) return;  // aesc_pull takes the pieces in dense depths
     const uint32_t lane = threadIdx.x & 31;
+    const bool need = ((active >> (2 * lane)) & 3ull) != 0;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < npieces;
          i += (gridDim.x * blockDim.x) >> 5) {
         const HeavyPiece pc = pieces[i];
         if (!dense && !flag[pc.row]) continue;
         double a0 = 0.0, a1 = 0.0;
         unsigned long long mask = 0;
-        pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, a0, a1, mask);
+        pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, need, a0, a1, mask);
         reinterpret_cast<double2*>(part + size_t(i) * kCols)[lane] = make_double2(a0, a1);
         if (lane == 0) part_mask[i] = mask;
     }
@@ -527,14 +543,28 @@ __global__ void aesc_clear(const uint32_t* __restrict__ tlist, const uint32_t* _
 
 // Walk phase layout. A slot's n_req pairs are split into groups of at most
 // kGroupPairs pairs; a chunk holds whole groups (<= kChunkWalks walks, both
-// sides). Within a chunk every walk gets the key (group << 16 | seed >> 16)
-// and one radix sort orders the chunk by group then seed: a warp then walks
-// 32 adjacent seeds of one (slot, side) — the SABA bouquet over the slot's
-// whole seed set, not just a tile (PAPER Alg. 3 + §3.3; walker.hpp:436-439).
+// sides). Walk w of a chunk is (group, side, k) in that order, so every
+// (group, side) "segment" is a contiguous range of walk ids.
+//
+// SABA bouquets (PAPER Alg. 3 + §3.3; walker.hpp:436-439): within each
+// segment the walks are bucketed by the top bits of their seeds, about 32
+// walks per bucket, so a warp walks 32 adjacent seeds of one (slot, side) —
+// the bouquet over the slot's whole seed set, not just a tile. The order is
+// a performance device only: every walk's score depends on its own seed and
+// lands in score[w], so any permutation gives identical results. That lets
+// the bucketing be a segment-local counting sort (K4s) instead of a global
+// radix sort: segments up to kFineDirect walks are bucketed by one CTA in
+// one pass; larger ones first split by their top d1 seed bits into coarse
+// buckets of about kCoarseTarget walks (count, scan, scatter), which the
+// same one-pass CTA then buckets by the next bits.
 constexpr uint32_t kGroupPairs = 1u << 24;
-constexpr uint32_t kSeedBits = 16;
 constexpr uint64_t kChunkWalks = uint64_t(1) << 28;
-constexpr uint32_t kPairTile = 2048;  // pairs per deterministic reduction tile
+constexpr uint32_t kPairTile = 2048;       // pairs per deterministic reduction tile
+constexpr uint32_t kFineDirect = 8192;     // segments up to this size skip the coarse split
+constexpr uint32_t kCoarseTarget = 6144;   // expected walks per coarse bucket (<= kFineStage)
+constexpr uint32_t kFineBitsMax = 11;      // <= 2048 fine buckets per coarse bucket
+constexpr uint32_t kCoarseTile = 8192;     // walks per CTA in the coarse passes
+constexpr uint32_t kCoarseBitsMax = 11;
 
 struct WalkGroup {
     uint64_t edge_seed;  // substream(src_seed, slot) (aesc.hpp:622)
@@ -557,36 +587,137 @@ struct SlotWork {
     uint32_t pad;
 };
 
-// sb = seed bits in the key: just enough that a seed bucket holds about a
-// warp's worth of walks of the chunk's largest group (finer buckets would
-// not make warps more coherent, coarser ones would); <= kSeedBits.
-// gid != nullptr: side-0 walks of one source (every slot of it starts at
-// v_i) share one bouquet keyed by the rho column, so they sort together
-// across slots; gid[w] then records each walk's group.
-__global__ void aesc_keygen(const WalkGroup* __restrict__ groups, const uint32_t* __restrict__ walk_offs,
-                            uint32_t ngroups, uint32_t nwalks, uint32_t sb, uint32_t* __restrict__ keys,
-                            uint32_t* __restrict__ vals, uint32_t* __restrict__ gid) {
-    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwalks; w += gridDim.x * blockDim.x) {
-        uint32_t lo = 0, hi = ngroups;  // walk_offs[g] <= w < walk_offs[g+1]
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (walk_offs[mid] <= w) lo = mid; else hi = mid;
-        }
-        const WalkGroup G = groups[lo];
-        const uint32_t local = w - G.walk_off;
-        const uint32_t side = local >= G.pairs;
-        const uint64_t k = G.k0 + (local - side * G.pairs);
-        // walk seed counter_hash(edge_seed, 2k+side) >> 32 (aesc.hpp:485)
-        const uint32_t seed = walk_seed(G.edge_seed, 2 * k + side);
-        if (gid) {
-            const uint32_t seg = side ? kCols + lo : G.col;
-            keys[w] = (seg << sb) | (seed >> (32 - sb));
-            gid[w] = lo;
-        } else {
-            // (group, side, seed top bits): each (slot, side) is its own bouquet set
-            keys[w] = (((lo << 1) | side) << sb) | (seed >> (32 - sb));
-        }
-        vals[w] = w;
+// One (group, side) segment of a chunk and its coarse buckets
+// [cb, cb + 2^d1) in the chunk's coarse-bucket table.
+struct SortSeg {
+    uint32_t group, side, start, size, d1, cb;
+};
+struct CoarseTile {
+    uint32_t seg, t0, count, pad;
+};
+
+// walk seed counter_hash(edge_seed, 2k+side) >> 32 (aesc.hpp:485) of walk w
+__device__ __forceinline__ uint32_t seed_of(const WalkGroup& G, uint32_t w) {
+    const uint32_t local = w - G.walk_off;
+    const uint32_t side = local >= G.pairs;
+    return walk_seed(G.edge_seed, 2 * (G.k0 + (local - side * G.pairs)) + side);
+}
+
+__device__ __forceinline__ uint32_t top_bits(uint32_t x, uint32_t skip, uint32_t bits) {
+    return bits ? uint32_t((uint64_t(x) << skip) & 0xffffffffull) >> (32 - bits) : 0u;
+}
+
+// K4s-1: per coarse tile, histogram of the top d1 seed bits (smem), flushed
+// with one global add per non-empty digit.
+__global__ void __launch_bounds__(512)
+    sort_coarse_count(const CoarseTile* __restrict__ tiles, const SortSeg* __restrict__ segs,
+                      const WalkGroup* __restrict__ groups, uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t hist[1u << kCoarseBitsMax];
+    const CoarseTile T = tiles[blockIdx.x];
+    const SortSeg S = segs[T.seg];
+    const WalkGroup G = groups[S.group];
+    const uint32_t nd = 1u << S.d1;
+    for (uint32_t d = threadIdx.x; d < nd; d += blockDim.x) hist[d] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < T.count; i += blockDim.x)
+        atomicAdd(hist + top_bits(seed_of(G, S.start + T.t0 + i), 0, S.d1), 1u);
+    __syncthreads();
+    for (uint32_t d = threadIdx.x; d < nd; d += blockDim.x)
+        if (hist[d]) atomicAdd(cnt + S.cb + d, hist[d]);
+}
+
+// K4s-2: same tiles; reserve one run per non-empty digit from the bucket
+// cursors, then place the tile's walk ids (order within a run is free).
+__global__ void __launch_bounds__(512)
+    sort_coarse_scatter(const CoarseTile* __restrict__ tiles, const SortSeg* __restrict__ segs,
+                        const WalkGroup* __restrict__ groups, uint32_t* __restrict__ cursor,
+                        uint32_t* __restrict__ tmp) {
+    __shared__ uint32_t hist[1u << kCoarseBitsMax], base[1u << kCoarseBitsMax];
+    const CoarseTile T = tiles[blockIdx.x];
+    const SortSeg S = segs[T.seg];
+    const WalkGroup G = groups[S.group];
+    const uint32_t nd = 1u << S.d1;
+    for (uint32_t d = threadIdx.x; d < nd; d += blockDim.x) hist[d] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < T.count; i += blockDim.x)
+        atomicAdd(hist + top_bits(seed_of(G, S.start + T.t0 + i), 0, S.d1), 1u);
+    __syncthreads();
+    for (uint32_t d = threadIdx.x; d < nd; d += blockDim.x) {
+        base[d] = hist[d] ? atomicAdd(cursor + S.cb + d, hist[d]) : 0u;
+        hist[d] = 0;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < T.count; i += blockDim.x) {
+        const uint32_t w = S.start + T.t0 + i;
+        const uint32_t d = top_bits(seed_of(G, w), 0, S.d1);
+        tmp[base[d] + atomicAdd(hist + d, 1u)] = w;
+    }
+}
+
+// K4s-3: one CTA per coarse bucket (a whole small segment, or one coarse
+// digit of a large one): counting sort by the next fine bits, about 32 walks
+// per fine bucket; writes the walk id and its group at the sorted position.
+// Buckets up to kFineStage walks are permuted in shared memory and written
+// out coalesced; the group id is the same for the whole bucket (a fill).
+constexpr uint32_t kFineStage = 9216;
+__global__ void __launch_bounds__(256)
+    sort_fine(const uint32_t* __restrict__ cb_seg, const SortSeg* __restrict__ segs,
+              const WalkGroup* __restrict__ groups, const uint32_t* __restrict__ cnt,
+              const uint32_t* __restrict__ start, const uint32_t* __restrict__ tmp,
+              uint32_t* __restrict__ out_w, uint32_t* __restrict__ out_g) {
+    using Scan = cub::BlockScan<uint32_t, 256>;
+    constexpr uint32_t kB = 1u << kFineBitsMax, kPer = kB / 256;
+    __shared__ uint32_t hist[kB];
+    __shared__ uint32_t stage[kFineStage];
+    __shared__ typename Scan::TempStorage scan_tmp;
+    const uint32_t b = blockIdx.x;
+    const uint32_t count = cnt[b];
+    if (count == 0) return;
+    const SortSeg S = segs[cb_seg[b]];
+    const WalkGroup G = groups[S.group];
+    const uint32_t at = start[b];
+    // about 32 walks per fine bucket
+    uint32_t fb = 0;
+    while (fb < kFineBitsMax && (32u << fb) < count) ++fb;
+    const uint32_t nf = 1u << fb;
+    for (uint32_t d = threadIdx.x; d < kB; d += blockDim.x) hist[d] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
+        const uint32_t w = S.d1 ? tmp[at + i] : S.start + i;
+        atomicAdd(hist + top_bits(seed_of(G, w), S.d1, fb), 1u);
+    }
+    __syncthreads();
+    // exclusive scan of hist[0, nf): kPer consecutive digits per thread
+    uint32_t v[kPer], run = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kPer; ++j) {
+        const uint32_t d = threadIdx.x * kPer + j;
+        v[j] = d < nf ? hist[d] : 0u;
+        run += v[j];
+    }
+    uint32_t excl;
+    Scan(scan_tmp).ExclusiveSum(run, excl);
+    __syncthreads();
+#pragma unroll
+    for (uint32_t j = 0; j < kPer; ++j) {
+        const uint32_t d = threadIdx.x * kPer + j;
+        if (d < nf) hist[d] = excl;
+        excl += v[j];
+    }
+    __syncthreads();
+    const bool staged = count <= kFineStage;
+    for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
+        const uint32_t w = S.d1 ? tmp[at + i] : S.start + i;
+        const uint32_t r = atomicAdd(hist + top_bits(seed_of(G, w), S.d1, fb), 1u);
+        if (staged)
+            stage[r] = w;
+        else
+            out_w[at + r] = w;
+    }
+    if (staged) __syncthreads();
+    for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
+        if (staged) out_w[at + i] = stage[i];
+        out_g[at + i] = S.group;
     }
 }
 
@@ -599,13 +730,13 @@ __global__ void aesc_keygen(const WalkGroup* __restrict__ groups, const uint32_t
 // so a step is one dependent gather (plus the rho gather, which feeds nothing).
 template <bool PACKED, int WPT, bool BITMAP, bool FAT>
 __global__ void __launch_bounds__(256)
-    aesc_walk_sorted(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+    aesc_walk_sorted(const uint32_t* __restrict__ gidx, const uint32_t* __restrict__ vals,
                      uint32_t nwalks, const WalkGroup* __restrict__ groups,
                      const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
                      const uint64_t* __restrict__ adjp, const double* __restrict__ R, uint32_t n,
                      const uint32_t* __restrict__ bits, uint32_t words, uint64_t mult,
-                     const uint64_t* __restrict__ fat, uint32_t fat_idb, uint32_t fat_sh, uint32_t sb,
-                     const uint32_t* __restrict__ gid, double* __restrict__ score) {
+                     const uint64_t* __restrict__ fat, uint32_t fat_idb, uint32_t fat_sh,
+                     double* __restrict__ score) {
     // Software-pipelined score side: the walk chain (csr -> adj, or one fat
     // gather) is the only dependency carried from step to step; the support
     // bit of x_l is loaded right after x_l is known, the rho gather of x_l is
@@ -632,7 +763,7 @@ __global__ void __launch_bounds__(256)
             bcol[r] = 0;
             if (e < nwalks) {
                 const uint32_t w = vals[e];
-                const WalkGroup G = groups[gid ? __ldg(gid + w) : keys[e] >> (sb + 1)];
+                const WalkGroup G = groups[gidx[e]];
                 const uint32_t local = w - G.walk_off;
                 const uint32_t side = local >= G.pairs;
                 seed[r] = walk_seed(G.edge_seed, 2 * (G.k0 + (local - side * G.pairs)) + side);
@@ -1005,20 +1136,11 @@ int bits_for(uint32_t x) {
     return b;
 }
 
-// Seed bits of the walk-sort key for a chunk whose largest bouquet has
-// max_pairs walks: about 32 walks per bucket, in [4, kSeedBits].
-uint32_t seed_bits(uint32_t max_pairs) {
-    return uint32_t(std::min<int>(kSeedBits, std::max(4, bits_for(max_pairs / 32) + 1)));
-}
-
 struct TileBuilder {
     struct Chunk {
         std::vector<WalkGroup> groups;
-        std::vector<uint32_t> offs;  // walk offsets + sentinel
         std::vector<PairTile> tiles;
         uint32_t walks = 0;
-        uint32_t max_pairs = 0;
-        uint32_t col_pairs[kCols] = {};  // side-0 walks per source column
     };
     std::vector<Chunk> chunks;
     std::vector<SlotWork> slots;
@@ -1037,25 +1159,13 @@ struct TileBuilder {
         const double inv_n = 1.0 / double(n_req);
         for (uint64_t k0 = 0; k0 < n_req; k0 += kGroupPairs) {
             const uint32_t pairs = uint32_t(std::min<uint64_t>(kGroupPairs, n_req - k0));
-            bool close = chunks.empty() || chunks.back().walks + 2ull * pairs > kChunkWalks ||
-                         chunks.back().groups.size() >= (1u << (31 - kSeedBits));
-            if (!close && chunks.back().walks >= (1u << 22)) {
-                // keep the (group, side, seed) key within 24 bits: 3 radix passes
-                const Chunk& c = chunks.back();
-                const int key_bits = int(seed_bits(std::max(c.max_pairs, pairs))) + 1 +
-                                     bits_for(uint32_t(c.groups.size()) + 1);
-                close = key_bits > 24;
-            }
-            if (close) chunks.emplace_back();
+            if (chunks.empty() || chunks.back().walks + 2ull * pairs > kChunkWalks) chunks.emplace_back();
             Chunk& c = chunks.back();
             const uint32_t gi = uint32_t(c.groups.size());
             c.groups.push_back({edge_seed, k0, pairs, c.walks, vi, vj, len, col});
-            c.offs.push_back(c.walks);
             for (uint32_t p0 = 0; p0 < pairs; p0 += kPairTile)
                 c.tiles.push_back({inv_n, gi, p0, std::min(kPairTile, pairs - p0), ntiles++});
             c.walks += 2 * pairs;
-            c.max_pairs = std::max(c.max_pairs, pairs);
-            c.col_pairs[col] += pairs;
         }
         w.t1 = ntiles;
         slots.push_back(w);
@@ -1073,6 +1183,75 @@ bool aesc_fat_enabled() {  // SABA_AESC_FAT=0 disables (default: on when L2-resi
     return on;
 }
 
+// K4s host side: segments of the chunk, coarse tiles and the coarse-bucket
+// table (a segment up to kFineDirect walks is one bucket), then count ->
+// exclusive scan -> scatter -> fine bucketing into (out_w, out_g).
+struct SortScratch {  // host side of one chunk's bucketing; lives until the chunk's sync
+    std::vector<SortSeg> segs;
+    std::vector<CoarseTile> ct;
+    std::vector<uint32_t> cnt0, cb_seg;  // initial counts (whole small segments), owner segment
+};
+void bucket_walks(AescState* st, cudaStream_t s, const TileBuilder::Chunk& c, const WalkGroup* dg,
+                  SortScratch& h, uint32_t* out_w, uint32_t* out_g, uint32_t* launches) {
+    const uint32_t nw = c.walks;
+    auto& segs = h.segs;
+    auto& ct = h.ct;
+    auto& cnt0 = h.cnt0;
+    auto& cb_seg = h.cb_seg;
+    segs.clear();
+    ct.clear();
+    cnt0.clear();
+    cb_seg.clear();
+    segs.reserve(2 * c.groups.size());
+    for (uint32_t gi = 0; gi < uint32_t(c.groups.size()); ++gi) {
+        const WalkGroup& G = c.groups[gi];
+        for (uint32_t side = 0; side < 2; ++side) {
+            SortSeg S{gi, side, G.walk_off + side * G.pairs, G.pairs, 0, uint32_t(cnt0.size())};
+            if (S.size > kFineDirect) {
+                while (S.d1 < kCoarseBitsMax && (uint64_t(kCoarseTarget) << S.d1) < S.size) ++S.d1;
+                for (uint32_t t0 = 0; t0 < S.size; t0 += kCoarseTile)
+                    ct.push_back({uint32_t(segs.size()), t0, std::min(kCoarseTile, S.size - t0), 0});
+            }
+            const uint32_t nb = 1u << S.d1;
+            cnt0.insert(cnt0.end(), nb, S.d1 ? 0u : S.size);
+            cb_seg.insert(cb_seg.end(), nb, uint32_t(segs.size()));
+            segs.push_back(S);
+        }
+    }
+    const uint32_t ncb = uint32_t(cnt0.size()), nseg = uint32_t(segs.size()), nct = uint32_t(ct.size());
+    auto* d_seg = static_cast<SortSeg*>(st->sort_segs.ensure(sizeof(SortSeg) * nseg));
+    auto* d_cbs = static_cast<uint32_t*>(st->cb_seg.ensure(sizeof(uint32_t) * ncb));
+    auto* d_cnt = static_cast<uint32_t*>(st->cb_cnt.ensure(sizeof(uint32_t) * ncb));
+    auto* d_start = static_cast<uint32_t*>(st->cb_start.ensure(sizeof(uint32_t) * ncb));
+    SABA_CUDA_CHECK(cudaMemcpyAsync(d_seg, segs.data(), sizeof(SortSeg) * nseg, cudaMemcpyHostToDevice, s));
+    SABA_CUDA_CHECK(cudaMemcpyAsync(d_cbs, cb_seg.data(), sizeof(uint32_t) * ncb, cudaMemcpyHostToDevice, s));
+    SABA_CUDA_CHECK(cudaMemcpyAsync(d_cnt, cnt0.data(), sizeof(uint32_t) * ncb, cudaMemcpyHostToDevice, s));
+    uint32_t* tmp = nullptr;
+    if (nct) {
+        auto* d_ct = static_cast<CoarseTile*>(st->coarse_tiles.ensure(sizeof(CoarseTile) * nct));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(d_ct, ct.data(), sizeof(CoarseTile) * nct, cudaMemcpyHostToDevice, s));
+        sort_coarse_count<<<nct, 512, 0, s>>>(d_ct, d_seg, dg, d_cnt);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        ++*launches;
+    }
+    size_t scan_bytes = 0;
+    SABA_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, d_cnt, d_start, int(ncb), s));
+    SABA_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(st->sort_tmp.ensure(scan_bytes), scan_bytes, d_cnt, d_start,
+                                                  int(ncb), s));
+    ++*launches;
+    if (nct) {
+        auto* d_cur = static_cast<uint32_t*>(st->cb_cursor.ensure(sizeof(uint32_t) * ncb));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(d_cur, d_start, sizeof(uint32_t) * ncb, cudaMemcpyDeviceToDevice, s));
+        tmp = static_cast<uint32_t*>(st->vals[1].ensure(sizeof(uint32_t) * nw));
+        sort_coarse_scatter<<<nct, 512, 0, s>>>(st->coarse_tiles.as<CoarseTile>(), d_seg, dg, d_cur, tmp);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        ++*launches;
+    }
+    sort_fine<<<ncb, 256, 0, s>>>(d_cbs, d_seg, dg, d_cnt, d_start, tmp, out_w, out_g);
+    SABA_CUDA_CHECK(cudaGetLastError());
+    ++*launches;
+}
+
 void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb, const double* R,
                const uint32_t* bits, uint64_t mult, double* g_hat_dev, uint32_t* launches) {
     const uint32_t words = (g->n + 31) / 32;
@@ -1085,46 +1264,23 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
     int occ = 0;
     SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk_sorted<false, WPT, true, true>,
                                                                   256, 0));
+    SortScratch scratch;
     for (TileBuilder::Chunk& c : tb.chunks) {
         const uint32_t ng = uint32_t(c.groups.size()), nw = c.walks, nt = uint32_t(c.tiles.size());
-        c.offs.push_back(nw);
         auto* dg = static_cast<WalkGroup*>(st->groups.ensure(sizeof(WalkGroup) * ng));
-        auto* doff = static_cast<uint32_t*>(st->woffs.ensure(sizeof(uint32_t) * (ng + 1)));
         auto* dt = static_cast<PairTile*>(st->tiles.ensure(sizeof(PairTile) * nt));
         SABA_CUDA_CHECK(cudaMemcpyAsync(dg, c.groups.data(), sizeof(WalkGroup) * ng, cudaMemcpyHostToDevice, s));
-        SABA_CUDA_CHECK(cudaMemcpyAsync(doff, c.offs.data(), sizeof(uint32_t) * (ng + 1), cudaMemcpyHostToDevice, s));
         SABA_CUDA_CHECK(cudaMemcpyAsync(dt, c.tiles.data(), sizeof(PairTile) * nt, cudaMemcpyHostToDevice, s));
-        cub::DoubleBuffer<uint32_t> keys(static_cast<uint32_t*>(st->keys[0].ensure(sizeof(uint32_t) * nw)),
-                                         static_cast<uint32_t*>(st->keys[1].ensure(sizeof(uint32_t) * nw)));
-        cub::DoubleBuffer<uint32_t> vals(static_cast<uint32_t*>(st->vals[0].ensure(sizeof(uint32_t) * nw)),
-                                         static_cast<uint32_t*>(st->vals[1].ensure(sizeof(uint32_t) * nw)));
+        uint32_t* out_g = static_cast<uint32_t*>(st->keys[0].ensure(sizeof(uint32_t) * nw));
+        uint32_t* out_w = static_cast<uint32_t*>(st->vals[0].ensure(sizeof(uint32_t) * nw));
         double* score = static_cast<double*>(st->score.ensure(sizeof(double) * nw));
-        static const bool merge = [] {  // SABA_AESC_MERGE=1: per-source side-0 bouquets
-            const char* e = getenv("SABA_AESC_MERGE");
-            return e && atoi(e) != 0;
-        }();
-        uint32_t max_seg = c.max_pairs;
-        if (merge)
-            for (uint32_t cp : c.col_pairs) max_seg = std::max(max_seg, cp);
-        uint32_t* gid = merge ? static_cast<uint32_t*>(st->gid.ensure(sizeof(uint32_t) * nw)) : nullptr;
-        const uint32_t sb = seed_bits(max_seg);
-        aesc_keygen<<<g->sm_count * 8, 256, 0, s>>>(dg, doff, ng, nw, sb, keys.Current(), vals.Current(), gid);
-        SABA_CUDA_CHECK(cudaGetLastError());
-        const int end_bit = merge ? int(sb) + std::max(1, bits_for(kCols + ng))
-                                  : int(sb) + 1 + std::max(1, bits_for(ng));
-        static const bool nosort = getenv("SABA_AESC_NOSORT") != nullptr;  // experiment knob
-        if (!nosort) {
-            size_t tmp = 0;
-            SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, int(nw), 0, end_bit, s));
-            void* t = st->sort_tmp.ensure(tmp);
-            SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(t, tmp, keys, vals, int(nw), 0, end_bit, s));
-        }
+        bucket_walks(st, s, c, dg, scratch, out_w, out_g, launches);
         const int grid = int(std::min<uint64_t>((nw + 32 * WPT - 1) / (32 * WPT) * 32 / 256 + 1,
                                                 uint64_t(g->sm_count) * std::max(occ, 1)));
 #define SABA_WALK_W(P, W, B, F)                                                                       \
-    aesc_walk_sorted<P, W, B, F><<<grid, 256, 0, s>>>(keys.Current(), vals.Current(), nw, dg, g->d_csr, \
-                                                      g->d_adj, g->d_adj_packed, R, g->n, bits, words,  \
-                                                      mult, g->d_adj_fat, g->fat_idb, g->fat_sh, sb, gid, score)
+    aesc_walk_sorted<P, W, B, F><<<grid, 256, 0, s>>>(out_g, out_w, nw, dg, g->d_csr, g->d_adj,         \
+                                                      g->d_adj_packed, R, g->n, bits, words, mult,      \
+                                                      g->d_adj_fat, g->fat_idb, g->fat_sh, score)
 #define SABA_WALK(P, B, F) SABA_WALK_W(P, WPT, B, F)
         static const int fat_wpt = [] {  // tuning knob SABA_AESC_WPT (fat path)
             const char* e = getenv("SABA_AESC_WPT");
@@ -1148,7 +1304,7 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         SABA_CUDA_CHECK(cudaGetLastError());
         aesc_pair_reduce<<<int(std::min<uint32_t>(nt, g->sm_count * 8)), 256, 0, s>>>(dt, nt, dg, score, part);
         SABA_CUDA_CHECK(cudaGetLastError());
-        *launches += 4;
+        *launches += 2;
         // the chunk's host metadata must outlive its uploads
         SABA_CUDA_CHECK(cudaStreamSynchronize(s));
     }
@@ -1165,23 +1321,39 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
 // device, rounding exactly like the host loop: y[u] = (sum in slot order of
 // x[a] * isd[a]) * isd[u], one multiply then one add per neighbour. The
 // sequential reductions stay on the host, so lambda_hat is bit-identical.
+// xs[a] = x[a] * isd[a], the rounded product every neighbour slot adds
+__global__ void plan_scale_kernel(const double* __restrict__ x, const double* __restrict__ isd,
+                                  double* __restrict__ xs, uint32_t n) {
+    for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x)
+        xs[a] = __dmul_rn(x[a], isd[a]);
+}
+
+// Warp per row: the lanes gather 32 neighbour products at a time (coalesced
+// adjacency, independent loads) and every lane then adds them one by one in
+// slot order, so the float64 sum is exactly the host loop's left fold while
+// no thread serialises a dependent load per neighbour.
 __global__ void plan_spmv_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
-                                 const double* __restrict__ x, const double* __restrict__ isd,
+                                 const double* __restrict__ xs, const double* __restrict__ isd,
                                  double* __restrict__ y, uint32_t n) {
-    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += nwarps) {
         const uint2 r = csr[u];
+        const uint32_t e = r.x + r.y;
         double acc = 0.0;
-        for (uint32_t s = r.x; s < r.x + r.y; ++s) {
-            const uint32_t a = adj[s];
-            acc = __dadd_rn(acc, __dmul_rn(x[a], isd[a]));
+        for (uint32_t s0 = r.x; s0 < e; s0 += 32) {
+            const uint32_t s = s0 + lane;
+            const double prod = s < e ? xs[adj[s]] : 0.0;
+            const uint32_t cnt = min(32u, e - s0);
+            for (uint32_t j = 0; j < cnt; ++j) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, prod, j));
         }
-        y[u] = __dmul_rn(acc, isd[u]);
+        if (lane == 0) y[u] = __dmul_rn(acc, isd[u]);
     }
 }
 
 struct DeviceSpmv {
     saba_cu_graph* g;
-    DevBuf x, isd, y;
+    DevBuf x, isd, y, xs;
     bool isd_up = false;
     SpmvFn fn() {
         return [this](const std::vector<double>& hx, const std::vector<double>& hisd, std::vector<double>& hy) {
@@ -1192,8 +1364,11 @@ struct DeviceSpmv {
                 isd_up = true;
             }
             copy_h2d(x.ensure(bytes), hx.data(), bytes, 0);
-            plan_spmv_kernel<<<(n + 255) / 256, 256>>>(g->d_csr, g->d_adj, x.as<double>(), isd.as<double>(),
-                                                       static_cast<double*>(y.ensure(bytes)), n);
+            const uint32_t grid = std::min<uint32_t>((n + 255) / 256, g->sm_count * 8);
+            double* d_xs = static_cast<double*>(xs.ensure(bytes));
+            plan_scale_kernel<<<grid, 256>>>(x.as<double>(), isd.as<double>(), d_xs, n);
+            plan_spmv_kernel<<<g->sm_count * 16, 256>>>(g->d_csr, g->d_adj, d_xs, isd.as<double>(),
+                                            static_cast<double*>(y.ensure(bytes)), n);
             SABA_CUDA_CHECK(cudaGetLastError());
             copy_d2h(hy.data(), y.p, bytes, 0);
         };

@@ -20,12 +20,7 @@
 #include "capi_util.hpp"
 #include "saba_hash.cuh"
 
-struct saba_hgraph {
-    uint32_t n = 0;
-    uint64_t m = 0;
-    std::vector<uint32_t> off;
-    std::vector<uint32_t> adj;
-};
+#include "hgraph.hpp"
 
 namespace saba_cu {
 
@@ -173,6 +168,65 @@ struct Lcg {
 };
 
 }  // namespace
+
+// Chung–Lu weights and the Vose alias table of the endpoint distribution;
+// shared by the host and device generators so both sample the same graph.
+void chung_lu_tables(uint32_t n, double gamma, double mean_degree, double max_degree, uint64_t seed,
+                     ChungLuTables& t) {
+    check_arg(n >= 2, "chung_lu: need n >= 2");
+    check_arg(gamma > 1.0, "chung_lu: gamma must be > 1");
+    check_arg(mean_degree > 0 && max_degree >= 1, "chung_lu: bad degree parameters");
+    const uint64_t s = substream(seed, 0x43484c55ull /*"CHLU"*/);
+    // weights: Pareto draws w = U^(-1/(gamma-1)), U in (0, 1]
+    std::vector<double> w(n);
+    const double ex = -1.0 / (gamma - 1.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < int64_t(n); ++i)
+        w[size_t(i)] = std::pow(1.0 - unit53(counter_hash(s, uint64_t(i))), ex);
+    // scale c such that the mean of the CAPPED weights min(c w, cap) is
+    // mean_degree (capping removes tail mass; bisection, deterministic)
+    auto capped_mean = [&](double c) {
+        double s = 0.0;
+        for (double x : w) s += std::min(x * c, max_degree);
+        return s / double(n);
+    };
+    double lo = 0.0, hi = 1.0;
+    while (capped_mean(hi) < mean_degree && hi < 1e30) hi *= 2.0;
+    check_arg(capped_mean(hi) >= mean_degree, "chung_lu: mean_degree unreachable under the cap");
+    for (int it = 0; it < 100; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        (capped_mean(mid) < mean_degree ? lo : hi) = mid;
+    }
+    const double scalef = hi;
+    double total = 0.0;
+    for (double& x : w) {
+        x = std::min(x * scalef, max_degree);
+        total += x;
+    }
+    // Vose alias table over w / total
+    std::vector<double> prob(n);
+    std::vector<uint32_t> alias(n, 0), small, large;
+    for (uint32_t i = 0; i < n; ++i) {
+        prob[i] = w[i] * double(n) / total;
+        (prob[i] < 1.0 ? small : large).push_back(i);
+    }
+    while (!small.empty() && !large.empty()) {
+        const uint32_t l = small.back(), g = large.back();
+        small.pop_back();
+        alias[l] = g;
+        prob[g] = (prob[g] + prob[l]) - 1.0;
+        if (prob[g] < 1.0) {
+            large.pop_back();
+            small.push_back(g);
+        }
+    }
+    for (uint32_t i : large) prob[i] = 1.0;
+    for (uint32_t i : small) prob[i] = 1.0;
+    t.prob = std::move(prob);
+    t.alias = std::move(alias);
+    t.samples = uint64_t(std::llround(total / 2.0));
+}
+
 }  // namespace saba_cu
 
 using namespace saba_cu;
@@ -241,32 +295,13 @@ int saba_gen_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, doub
         check_arg(edge_factor >= 1, "rmat: edge_factor must be >= 1");
         check_arg(a > 0 && b >= 0 && c >= 0 && a + b + c < 1.0, "rmat: bad quadrant probabilities");
         const uint64_t samples = uint64_t(edge_factor) << scale;
-        const uint64_t s = substream(seed, 0x524d4154ull /*"RMAT"*/);
-        // quadrant thresholds on a 32-bit uniform
-        const double two32 = 4294967296.0;
-        const uint64_t ta = uint64_t(a * two32), tb = uint64_t((a + b) * two32),
-                       tc = uint64_t((a + b + c) * two32);
+        const uint64_t s = substream(seed, kRmatTag);
+        const RmatThresholds thr = rmat_thresholds(a, b, c);
         std::vector<uint64_t> keys(samples);
 #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < int64_t(samples); ++i) {
-            uint32_t u = 0, v = 0;
-            const uint64_t si = counter_hash(s, uint64_t(i));
-            for (uint32_t lvl = 0; lvl < scale; lvl += 2) {
-                const uint64_t h = counter_hash(si, lvl);
-                for (uint32_t q = 0; q < 2 && lvl + q < scale; ++q) {
-                    const uint64_t r = q ? (h & 0xffffffffu) : (h >> 32);
-                    const uint32_t bit = 1u << (scale - 1 - (lvl + q));
-                    if (r < ta) {
-                    } else if (r < tb) {
-                        v |= bit;
-                    } else if (r < tc) {
-                        u |= bit;
-                    } else {
-                        u |= bit;
-                        v |= bit;
-                    }
-                }
-            }
+            uint32_t u, v;
+            rmat_sample(s, uint64_t(i), scale, thr, u, v);
             keys[size_t(i)] = pack(u, v);
         }
         *out = maybe_lcc(from_pairs(uint32_t(1u << scale), keys), keep_lcc);
@@ -277,69 +312,17 @@ int saba_gen_chung_lu(uint32_t n, double gamma, double mean_degree, double max_d
                       uint64_t seed, int keep_lcc, saba_hgraph** out) {
     return guard([&] {
         check_arg(out != nullptr, "null output");
-        check_arg(n >= 2, "chung_lu: need n >= 2");
-        check_arg(gamma > 1.0, "chung_lu: gamma must be > 1");
-        check_arg(mean_degree > 0 && max_degree >= 1, "chung_lu: bad degree parameters");
-        const uint64_t s = substream(seed, 0x43484c55ull /*"CHLU"*/);
-        // weights: Pareto draws w = U^(-1/(gamma-1)), U in (0, 1]
-        std::vector<double> w(n);
-        const double ex = -1.0 / (gamma - 1.0);
-#pragma omp parallel for schedule(static)
-        for (int64_t i = 0; i < int64_t(n); ++i)
-            w[size_t(i)] = std::pow(1.0 - unit53(counter_hash(s, uint64_t(i))), ex);
-        // scale c such that the mean of the CAPPED weights min(c w, cap) is
-        // mean_degree (capping removes tail mass; bisection, deterministic)
-        auto capped_mean = [&](double c) {
-            double s = 0.0;
-            for (double x : w) s += std::min(x * c, max_degree);
-            return s / double(n);
-        };
-        double lo = 0.0, hi = 1.0;
-        while (capped_mean(hi) < mean_degree && hi < 1e30) hi *= 2.0;
-        check_arg(capped_mean(hi) >= mean_degree, "chung_lu: mean_degree unreachable under the cap");
-        for (int it = 0; it < 100; ++it) {
-            const double mid = 0.5 * (lo + hi);
-            (capped_mean(mid) < mean_degree ? lo : hi) = mid;
-        }
-        const double scalef = hi;
-        double total = 0.0;
-        for (double& x : w) {
-            x = std::min(x * scalef, max_degree);
-            total += x;
-        }
-        // Vose alias table over w / total
-        std::vector<double> prob(n);
-        std::vector<uint32_t> alias(n, 0), small, large;
-        for (uint32_t i = 0; i < n; ++i) {
-            prob[i] = w[i] * double(n) / total;
-            (prob[i] < 1.0 ? small : large).push_back(i);
-        }
-        while (!small.empty() && !large.empty()) {
-            const uint32_t l = small.back(), g = large.back();
-            small.pop_back();
-            alias[l] = g;
-            prob[g] = (prob[g] + prob[l]) - 1.0;
-            if (prob[g] < 1.0) {
-                large.pop_back();
-                small.push_back(g);
-            }
-        }
-        for (uint32_t i : large) prob[i] = 1.0;
-        for (uint32_t i : small) prob[i] = 1.0;
-        const uint64_t samples = uint64_t(std::llround(total / 2.0));
-        const uint64_t s2 = substream(seed, 0x43484c32ull);
+        ChungLuTables t;
+        chung_lu_tables(n, gamma, mean_degree, max_degree, seed, t);
+        const std::vector<double>& prob = t.prob;
+        const std::vector<uint32_t>& alias = t.alias;
+        const uint64_t samples = t.samples;
+        const uint64_t s2 = substream(seed, kChungLuTag);
         std::vector<uint64_t> keys(samples);
 #pragma omp parallel for schedule(static)
-        for (int64_t i = 0; i < int64_t(samples); ++i) {
-            uint32_t ends[2];
-            for (int e = 0; e < 2; ++e) {
-                const uint64_t h = counter_hash(s2, 2 * uint64_t(i) + e);
-                const uint32_t col = scaled_index(uint32_t(h >> 32), n);
-                const double coin = double(uint32_t(h)) * 0x1.0p-32;
-                ends[e] = coin < prob[col] ? col : alias[col];
-            }
-            keys[size_t(i)] = pack(ends[0], ends[1]);
-        }
+        for (int64_t i = 0; i < int64_t(samples); ++i)
+            keys[size_t(i)] = pack(chung_lu_end(s2, uint64_t(i), 0, n, prob.data(), alias.data()),
+                                   chung_lu_end(s2, uint64_t(i), 1, n, prob.data(), alias.data()));
         *out = maybe_lcc(from_pairs(n, keys), keep_lcc);
     });
 }

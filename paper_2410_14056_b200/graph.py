@@ -50,9 +50,16 @@ class Graph:
 
     # -- construction (graph.hpp:86-105; gen.hpp; BASELINE generators)
     @staticmethod
-    def from_edges(n_hint: int, pairs) -> "Graph":
+    def from_edges(n_hint: int, pairs, device: int | None = None, keep_lcc: bool = False) -> "Graph":
+        """graph.hpp:86-105. device=None canonicalises on the host; a CUDA
+        device index runs the device pipeline (graph_build.cu), which returns
+        the identical CSR; keep_lcc additionally keeps the largest component."""
         p = np.ascontiguousarray(np.asarray(pairs, dtype=np.uint32).reshape(-1, 2))
-        return _gen(L.lib().saba_hgraph_from_edges, n_hint, L.ptr(p, L.u32p), len(p))
+        if device is not None:
+            return _gen(L.lib().saba_cu_graph_from_edges, n_hint, L.ptr(p, L.u32p), len(p),
+                        int(keep_lcc), int(device))
+        g = _gen(L.lib().saba_hgraph_from_edges, n_hint, L.ptr(p, L.u32p), len(p))
+        return largest_component(g) if keep_lcc else g
 
     @staticmethod
     def from_csr(offsets, adjacency) -> "Graph":
@@ -166,14 +173,23 @@ def make_erdos_renyi(n: int, m: int, seed: int) -> Graph:
 
 
 def make_rmat(scale: int, edge_factor: int, a: float = 0.57, b: float = 0.19, c: float = 0.19,
-              seed: int = 1, keep_lcc: bool = True) -> Graph:
-    """R-MAT, symmetrised/deduplicated/loop-free, LCC (BASELINE configs 2-4)."""
+              seed: int = 1, keep_lcc: bool = True, device: int | None = None) -> Graph:
+    """R-MAT, symmetrised/deduplicated/loop-free, LCC (BASELINE configs 2-4).
+    device: build on that CUDA device (same graph, bit for bit)."""
+    if device is not None:
+        return _gen(L.lib().saba_cu_gen_rmat, scale, edge_factor, a, b, c, seed, int(keep_lcc),
+                    int(device))
     return _gen(L.lib().saba_gen_rmat, scale, edge_factor, a, b, c, seed, int(keep_lcc))
 
 
 def make_chung_lu(n: int, gamma: float = 2.2, mean_degree: float = 78.0,
-                  max_degree: float = 30000.0, seed: int = 1, keep_lcc: bool = True) -> Graph:
-    """Chung–Lu power law, LCC (BASELINE config 5)."""
+                  max_degree: float = 30000.0, seed: int = 1, keep_lcc: bool = True,
+                  device: int | None = None) -> Graph:
+    """Chung–Lu power law, LCC (BASELINE config 5). device: build on that CUDA
+    device (alias table on the host, samples/canonicalisation/LCC on the GPU)."""
+    if device is not None:
+        return _gen(L.lib().saba_cu_gen_chung_lu, n, gamma, mean_degree, max_degree, seed,
+                    int(keep_lcc), int(device))
     return _gen(L.lib().saba_gen_chung_lu, n, gamma, mean_degree, max_degree, seed, int(keep_lcc))
 
 

@@ -81,6 +81,15 @@ static void host_checks() {
 
 static void gpu_checks() {
     const Graph f = fig1();
+    // device canonicalisation == host canonicalisation (graph.hpp:86-105):
+    // loops, reversed and repeated pairs, an isolated tail vertex
+    {
+        const std::vector<std::pair<uint32_t, uint32_t>> messy = {
+            {3, 1}, {1, 3}, {2, 2}, {0, 4}, {4, 0}, {4, 0}, {1, 4}, {5, 5}, {2, 1}};
+        const Graph h = Graph::from_edges(7, messy), d = Graph::from_edges(7, messy, 0);
+        CHECK(d.vertex_count() == 7 && d.edge_count() == h.edge_count());
+        CHECK(d.offsets() == h.offsets() && d.adjacency() == h.adjacency());
+    }
     // test_walker.cpp:49-75
     CHECK(random_walk(f, 2, 1, SelectorKind::Scaled, 77).vertices == std::vector<uint32_t>{2});
     CHECK(random_walk(path(2), 0, 3, SelectorKind::Scaled, 123).vertices ==
