@@ -59,7 +59,16 @@
 namespace saba_cu {
 
 constexpr int kCols = 64;           // sources per propagation batch
-constexpr int kDepthsPerGraph = 4;  // propagation depths per CUDA-graph replay
+// propagation depths per CUDA-graph replay (even); SABA_DEPTHS_PER_GRAPH
+// overrides (tuning knob)
+int depths_per_graph() {
+    static const int d = [] {
+        const char* e = getenv("SABA_DEPTHS_PER_GRAPH");
+        const int v = e ? atoi(e) : 4;
+        return std::max(2, v + (v & 1));
+    }();
+    return d;
+}
 
 struct AescState {
     uint32_t n_cap = 0;
@@ -728,8 +737,11 @@ __global__ void __launch_bounds__(256)
 // (adding +0.0 is the identity, so scores are unchanged).
 // FAT: slots carry the neighbour's {id, base, degree} (L2-resident graphs),
 // so a step is one dependent gather (plus the rho gather, which feeds nothing).
-template <bool PACKED, int WPT, bool BITMAP, bool FAT>
-__global__ void __launch_bounds__(256)
+// WPT walks per lane, MINB resident blocks per SM (register budget): short
+// walks are prologue/latency bound and want many warps with 2 walks each
+// (32 registers), long ones 4 walks per lane (48 registers); see run_tiles.
+template <bool PACKED, int WPT, bool BITMAP, bool FAT, int MINB>
+__global__ void __launch_bounds__(256, MINB)
     aesc_walk_sorted(const uint32_t* __restrict__ gidx, const uint32_t* __restrict__ vals,
                      uint32_t nwalks, const WalkGroup* __restrict__ groups,
                      const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
@@ -892,7 +904,7 @@ struct Engine {
     SlotTau tau_slot;  // tau per directed slot (host side)
     uint32_t launches = 0;
     uint64_t pairs = 0, steps = 0;
-    cudaGraphExec_t depth_graph = nullptr;  // kDepthsPerGraph captured depths
+    cudaGraphExec_t depth_graph = nullptr;  // depths_per_graph() captured depths
 
     ~Engine() {
         if (depth_graph) cudaGraphExecDestroy(depth_graph);
@@ -1069,20 +1081,20 @@ struct Engine {
         };
         const uint32_t per_depth = st->npieces ? 7 : 5;
         if (!depth_graph) {
-            // kDepthsPerGraph depths (even, so the buffer parity returns to 0)
+            // depths_per_graph() depths (even, so the buffer parity returns to 0)
             // captured once per estimator call and replayed for every batch
             cudaGraph_t graph;
             SABA_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-            for (int d = 0; d < kDepthsPerGraph; ++d) enqueue_depth(d & 1);
+            for (int d = 0; d < depths_per_graph(); ++d) enqueue_depth(d & 1);
             SABA_CUDA_CHECK(cudaStreamEndCapture(s, &graph));
             SABA_CUDA_CHECK(cudaGraphInstantiate(&depth_graph, graph, 0));
             SABA_CUDA_CHECK(cudaGraphDestroy(graph));
         }
         // columns freeze at the latest when l reaches tau_src <= lmax; extra
         // depths of the last replay only run early-exiting kernels
-        for (uint32_t l = 0; l <= lmax; l += kDepthsPerGraph) {
+        for (uint32_t l = 0; l <= lmax; l += depths_per_graph()) {
             SABA_CUDA_CHECK(cudaGraphLaunch(depth_graph, s));
-            launches += per_depth * kDepthsPerGraph;
+            launches += per_depth * depths_per_graph();
             if (read_ctrl(kActive) == 0) break;
         }
         SABA_CUDA_CHECK(cudaGetLastError());
@@ -1141,6 +1153,7 @@ struct TileBuilder {
         std::vector<WalkGroup> groups;
         std::vector<PairTile> tiles;
         uint32_t walks = 0;
+        uint64_t steps = 0;  // walk steps of the chunk (both sides)
     };
     std::vector<Chunk> chunks;
     std::vector<SlotWork> slots;
@@ -1166,6 +1179,7 @@ struct TileBuilder {
             for (uint32_t p0 = 0; p0 < pairs; p0 += kPairTile)
                 c.tiles.push_back({inv_n, gi, p0, std::min(kPairTile, pairs - p0), ntiles++});
             c.walks += 2 * pairs;
+            c.steps += 2ull * pairs * (len - 1);
         }
         w.t1 = ntiles;
         slots.push_back(w);
@@ -1252,6 +1266,43 @@ void bucket_walks(AescState* st, cudaStream_t s, const TileBuilder::Chunk& c, co
     ++*launches;
 }
 
+struct Launch {
+    const uint32_t *out_g, *out_w;
+    uint32_t nw;
+    const WalkGroup* dg;
+    const saba_cu_graph* g;
+    const double* R;
+    const uint32_t* bits;
+    uint32_t words;
+    uint64_t mult;
+    double* score;
+    cudaStream_t s;
+};
+
+template <bool P, int WPT, bool B, bool F, int MINB>
+void walk_launch(const Launch& L) {
+    auto k = aesc_walk_sorted<P, WPT, B, F, MINB>;
+    int occ = 0;
+    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0));
+    const int grid = int(std::min<uint64_t>((uint64_t(L.nw) + 32 * WPT - 1) / (32 * WPT) * 32 / 256 + 1,
+                                            uint64_t(L.g->sm_count) * std::max(occ, 1)));
+    k<<<grid, 256, 0, L.s>>>(L.out_g, L.out_w, L.nw, L.dg, L.g->d_csr, L.g->d_adj, L.g->d_adj_packed, L.R,
+                             L.g->n, L.bits, L.words, L.mult, L.g->d_adj_fat, L.g->fat_idb, L.g->fat_sh,
+                             L.score);
+}
+
+template <int WPT, int MINB>
+void walk_dispatch(const Launch& L, bool fat, bool packed) {
+    const bool b = L.bits != nullptr;
+    if (fat) {
+        if (b) walk_launch<false, WPT, true, true, MINB>(L); else walk_launch<false, WPT, false, true, MINB>(L);
+    } else if (packed) {
+        if (b) walk_launch<true, WPT, true, false, MINB>(L); else walk_launch<true, WPT, false, false, MINB>(L);
+    } else {
+        if (b) walk_launch<false, WPT, true, false, MINB>(L); else walk_launch<false, WPT, false, false, MINB>(L);
+    }
+}
+
 void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb, const double* R,
                const uint32_t* bits, uint64_t mult, double* g_hat_dev, uint32_t* launches) {
     const uint32_t words = (g->n + 31) / 32;
@@ -1260,10 +1311,6 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
     const bool packed = g->d_adj_packed != nullptr;
     // the fat adjacency is built (main thread) before any batch worker runs
     const bool fat = g->d_adj_fat != nullptr && fat_fits_l2(g) && aesc_fat_enabled();
-    constexpr int WPT = 4;
-    int occ = 0;
-    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aesc_walk_sorted<false, WPT, true, true>,
-                                                                  256, 0));
     SortScratch scratch;
     for (TileBuilder::Chunk& c : tb.chunks) {
         const uint32_t ng = uint32_t(c.groups.size()), nw = c.walks, nt = uint32_t(c.tiles.size());
@@ -1275,32 +1322,15 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         uint32_t* out_w = static_cast<uint32_t*>(st->vals[0].ensure(sizeof(uint32_t) * nw));
         double* score = static_cast<double*>(st->score.ensure(sizeof(double) * nw));
         bucket_walks(st, s, c, dg, scratch, out_w, out_g, launches);
-        const int grid = int(std::min<uint64_t>((nw + 32 * WPT - 1) / (32 * WPT) * 32 / 256 + 1,
-                                                uint64_t(g->sm_count) * std::max(occ, 1)));
-#define SABA_WALK_W(P, W, B, F)                                                                       \
-    aesc_walk_sorted<P, W, B, F><<<grid, 256, 0, s>>>(out_g, out_w, nw, dg, g->d_csr, g->d_adj,         \
-                                                      g->d_adj_packed, R, g->n, bits, words, mult,      \
-                                                      g->d_adj_fat, g->fat_idb, g->fat_sh, score)
-#define SABA_WALK(P, B, F) SABA_WALK_W(P, WPT, B, F)
-        static const int fat_wpt = [] {  // tuning knob SABA_AESC_WPT (fat path)
-            const char* e = getenv("SABA_AESC_WPT");
-            return e ? atoi(e) : 4;
-        }();
-        if (fat) {
-            if (fat_wpt == 8) {
-                if (bits) SABA_WALK_W(false, 8, true, true); else SABA_WALK_W(false, 8, false, true);
-            } else if (fat_wpt == 2) {
-                if (bits) SABA_WALK_W(false, 2, true, true); else SABA_WALK_W(false, 2, false, true);
-            } else {
-                if (bits) SABA_WALK(false, true, true); else SABA_WALK(false, false, true);
-            }
-        } else if (packed) {
-            if (bits) SABA_WALK(true, true, false); else SABA_WALK(true, false, false);
-        } else {
-            if (bits) SABA_WALK(false, true, false); else SABA_WALK(false, false, false);
-        }
-#undef SABA_WALK
-#undef SABA_WALK_W
+        // walk shape of the chunk: mean steps per walk decides the variant
+        // (measured: cfg5, ~12 steps, 2 x 8 beats 4 x 5 by 12%; cfg3/cfg4,
+        // 24-73 steps, 4 x 5 is best by 3-4%)
+        const bool short_walks = c.steps < 20ull * nw;
+        const Launch L{out_g, out_w, nw, dg, g, R, bits, words, mult, score, s};
+        if (short_walks)
+            walk_dispatch<2, 8>(L, fat, packed);
+        else
+            walk_dispatch<4, 5>(L, fat, packed);
         SABA_CUDA_CHECK(cudaGetLastError());
         aesc_pair_reduce<<<int(std::min<uint32_t>(nt, g->sm_count * 8)), 256, 0, s>>>(dt, nt, dg, score, part);
         SABA_CUDA_CHECK(cudaGetLastError());
