@@ -64,7 +64,7 @@ constexpr int kCols = 64;           // sources per propagation batch
 int depths_per_graph() {
     static const int d = [] {
         const char* e = getenv("SABA_DEPTHS_PER_GRAPH");
-        const int v = e ? atoi(e) : 4;
+        const int v = e ? atoi(e) : 8;
         return std::max(2, v + (v & 1));
     }();
     return d;
@@ -226,7 +226,7 @@ __global__ void aesc_check(uint32_t* __restrict__ ucount_next, const uint32_t* _
         // depth sees the same mode
         if (ctrl[kDenseReq]) ctrl[kDense] = 1;
         ctrl[kDepth] = l + 1;
-        ctrl[kRowNext] = 0;  // dense pull: next row of the degree-ordered list
+        ctrl[kRowNext] = 0;  // dense pull: next item of the degree-ordered work list
         *ucount_next = 0;
     }
 }
@@ -255,6 +255,18 @@ __global__ void aesc_rho(const double* __restrict__ P, const uint2* __restrict__
     }
 }
 
+// list[count++] = x for every lane with `take`, one atomic per warp (all 32
+// lanes must call).
+__device__ __forceinline__ void warp_append(uint32_t* __restrict__ list, uint32_t* __restrict__ count,
+                                            uint32_t x, bool take, uint32_t lane) {
+    const uint32_t m = __ballot_sync(0xffffffffu, take);
+    if (!m) return;
+    uint32_t base = 0;
+    if (lane == uint32_t(__ffs(m) - 1)) base = atomicAdd(count, uint32_t(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (take) list[base + __popc(m & ((1u << lane) - 1u))] = x;
+}
+
 // Sparse frontier growth: rows of depth l+1 = N(rows of depth l that still
 // carry an active column). Warp per row; the order of the new list is
 // irrelevant (every row is computed independently).
@@ -274,14 +286,23 @@ __global__ void aesc_expand(const uint2* __restrict__ csr, const uint32_t* __res
         const uint32_t v = ulist[i];
         if (!(M[v] & active)) continue;
         const uint2 r = csr[v];
-        for (uint32_t s = r.x + lane; s < r.x + r.y; s += 32) {
-            const uint32_t x = adj[s];
-            if (flag[x] || atomicExch(flag + x, 1u)) continue;
-            ulist_next[atomicAdd(ucount_next, 1u)] = x;
-            if (!tflag[x]) {  // x is claimed by exactly one thread per depth
-                tflag[x] = 1;
-                tlist[atomicAdd(tcount, 1u)] = x;
+        for (uint32_t s0 = r.x; s0 < r.x + r.y; s0 += 32) {
+            const uint32_t s = s0 + lane;
+            uint32_t x = 0;
+            bool claim = false;
+            if (s < r.x + r.y) {
+                x = adj[s];
+                claim = !flag[x] && !atomicExch(flag + x, 1u);
             }
+            // appends are warp-aggregated: one counter atomic per warp, not
+            // per row (a single global counter serialises in L2)
+            warp_append(ulist_next, ucount_next, x, claim, lane);
+            bool fresh = false;
+            if (claim && !tflag[x]) {  // x is claimed by exactly one thread per depth
+                tflag[x] = 1;
+                fresh = true;
+            }
+            warp_append(tlist, tcount, x, fresh, lane);
         }
     }
 }
@@ -398,29 +419,32 @@ __global__ void __launch_bounds__(256, SABA_PULL_MINB)
     const bool need = ((active >> (2 * lane)) & 3ull) != 0;
     unsigned long long ds0 = 0, ds1 = 0;
     if (dense && light_order) {
-        // dense depths: hub-row pieces, then light rows in descending degree
-        // order, handed out one at a time (longest first), so no warp is
-        // left with a long tail; aesc_pull_combine folds the pieces after
-        for (;;) {
-            uint32_t i = 0;
-            if (lane == 0) i = uint32_t(atomicAdd(ctrl + kRowNext, 1ull));
-            i = __shfl_sync(0xffffffffu, i, 0);
-            if (i >= npieces + nlight) break;
+        // dense depths: one work list of hub-row pieces, then light rows in
+        // descending degree order, handed out one item at a time (longest
+        // first, so no warp is left with a long tail); the next item is
+        // claimed before the current one is summed, which hides the counter
+        // atomic's round trip; aesc_pull_combine folds the pieces after
+        const uint32_t total = npieces + nlight;
+        uint32_t i = 0;
+        if (lane == 0) i = uint32_t(atomicAdd(ctrl + kRowNext, 1ull));
+        i = __shfl_sync(0xffffffffu, i, 0);
+        while (i < total) {
+            uint32_t nxt = 0;
+            if (lane == 0) nxt = uint32_t(atomicAdd(ctrl + kRowNext, 1ull));
+            double a0 = 0.0, a1 = 0.0;
+            unsigned long long mask = 0;
             if (i < npieces) {
                 const HeavyPiece pc = pieces[i];
-                double a0 = 0.0, a1 = 0.0;
-                unsigned long long mask = 0;
                 pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, need, a0, a1, mask);
                 reinterpret_cast<double2*>(part + size_t(i) * kCols)[lane] = make_double2(a0, a1);
                 if (lane == 0) part_mask[i] = mask;
-                continue;
+            } else {
+                const uint32_t x = light_order[i - npieces];
+                const uint2 r = csr[x];
+                pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, need, a0, a1, mask);
+                pull_store(x, r.y, a0, a1, mask, active, lane, Pn, Qn, Mn, ds0, ds1);
             }
-            const uint32_t x = light_order[i - npieces];
-            const uint2 r = csr[x];
-            double a0 = 0.0, a1 = 0.0;
-            unsigned long long mask = 0;
-            pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, need, a0, a1, mask);
-            pull_store(x, r.y, a0, a1, mask, active, lane, Pn, Qn, Mn, ds0, ds1);
+            i = __shfl_sync(0xffffffffu, nxt, 0);
         }
         flush_degsum(bds, ds0, ds1, lane, degsum_next);
         return;
