@@ -37,6 +37,11 @@ def test_no_cpu_fallback(sb, gpu_available):
         sb.random_walk(g, 0, 3, sb.SelectorKind.Scaled, 1)
     with pytest.raises(sb.CudaError):
         sb.run_walk_campaign(g, sb.CampaignConfig(walks_per_vertex=1, length=2), sb.VisitCountSink(3))
+    # device graph ingest does not quietly fall back to the host builder either
+    with pytest.raises(sb.CudaError):
+        sb.Graph.from_edges(3, [(0, 1), (1, 2)], device=0)
+    with pytest.raises(sb.CudaError):
+        sb.make_rmat(8, 4, seed=1, device=0)
 
 
 def test_named_graph_csr_matches_reference(golden, sb):
