@@ -503,7 +503,7 @@ def run_aesc_bench(args):
                        "l2": "working set per step exceeds L2 (cfg4/5) or is re-read in full per depth"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": "walk phase (keygen+sort+aesc_walk_sorted+pair_reduce)",
+                         "kernel": "walk phase (K4s bucketing + aesc_walk_sorted + pair_reduce)",
                          "bytes_per_step": 96, "peak_source": peak_src,
                          "note": "per-lane accounting; SABA-sorted warps share most gathers, so frac can exceed 1"},
             "cpu_baseline": cpu,
