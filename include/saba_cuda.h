@@ -96,6 +96,8 @@ SABA_API int saba_cu_gen_chung_lu(uint32_t n, double gamma, double mean_degree, 
                                   uint64_t seed, int keep_lcc, int device, saba_hgraph** out);
 SABA_API uint32_t saba_hgraph_vertex_count(const saba_hgraph* g);
 SABA_API uint64_t saba_hgraph_edge_count(const saba_hgraph* g);
+/* borrow the handle's offsets[n+1] / adjacency[2m] (valid until saba_hgraph_free) */
+SABA_API int saba_hgraph_data(const saba_hgraph* g, const uint32_t** offsets, const uint32_t** adjacency);
 /* copy out offsets[n+1] and adjacency[2m] */
 SABA_API int saba_hgraph_csr(const saba_hgraph* g, uint32_t* offsets, uint32_t* adjacency);
 SABA_API void saba_hgraph_free(saba_hgraph* g);

@@ -83,6 +83,7 @@ SIGNATURES = {
     "saba_hgraph_vertex_count": (C.c_uint32, [vp]),
     "saba_hgraph_edge_count": (C.c_uint64, [vp]),
     "saba_hgraph_csr": (C.c_int, [vp, u32p, u32p]),
+    "saba_hgraph_data": (C.c_int, [vp, C.POINTER(u32p), C.POINTER(u32p)]),
     "saba_hgraph_free": (None, [vp]),
     "saba_cu_graph_create": (C.c_int, [u32p, u32p, C.c_uint32, C.c_uint64, C.c_int, vpp]),
     "saba_cu_graph_destroy": (C.c_int, [vp]),

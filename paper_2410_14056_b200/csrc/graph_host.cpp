@@ -104,6 +104,18 @@ saba_hgraph* from_pairs(uint32_t n_hint, std::vector<uint64_t>& keys) {
     return csr_from_sorted_keys(n, keys);
 }
 
+// Large copies out of a graph land in fresh caller pages: fault them in on
+// every core, not one.
+void par_copy(uint32_t* dst, const uint32_t* src, size_t count) {
+    constexpr size_t kPiece = size_t(1) << 18;
+    const int64_t pieces = int64_t((count + kPiece - 1) / kPiece);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < pieces; ++i) {
+        const size_t o = size_t(i) * kPiece;
+        std::memcpy(dst + o, src + o, sizeof(uint32_t) * std::min(kPiece, count - o));
+    }
+}
+
 inline uint64_t pack(uint32_t a, uint32_t b) {
     if (a > b) std::swap(a, b);
     return (uint64_t(a) << 32) | b;
@@ -390,14 +402,22 @@ int saba_hgraph_largest_component(const saba_hgraph* in, saba_hgraph** out) {
     });
 }
 
+int saba_hgraph_data(const saba_hgraph* g, const uint32_t** offsets, const uint32_t** adjacency) {
+    return guard([&] {
+        check_arg(g && offsets && adjacency, "null argument");
+        *offsets = g->off.data();
+        *adjacency = g->adj.data();
+    });
+}
+
 uint32_t saba_hgraph_vertex_count(const saba_hgraph* g) { return g ? g->n : 0; }
 uint64_t saba_hgraph_edge_count(const saba_hgraph* g) { return g ? g->m : 0; }
 
 int saba_hgraph_csr(const saba_hgraph* g, uint32_t* offsets, uint32_t* adjacency) {
     return guard([&] {
         check_arg(g && offsets && adjacency, "null argument");
-        std::memcpy(offsets, g->off.data(), sizeof(uint32_t) * g->off.size());
-        std::memcpy(adjacency, g->adj.data(), sizeof(uint32_t) * g->adj.size());
+        par_copy(offsets, g->off.data(), g->off.size());
+        par_copy(adjacency, g->adj.data(), g->adj.size());
     });
 }
 

@@ -2,15 +2,42 @@
 // the CPU, graph_build.cu on the device) and the generator tables both share.
 #pragma once
 #include <cstdint>
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "saba_hash.cuh"
 
+namespace saba_cu {
+// resize() without value-initialisation: the CSR arrays are always fully
+// written after sizing, and zero-filling ~1 GB on one thread (plus its page
+// faults) cost more than building the whole graph on the device.
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = UninitAlloc<U>;
+    };
+    UninitAlloc() = default;
+    template <class U>
+    UninitAlloc(const UninitAlloc<U>&) noexcept {}
+    template <class U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <class U, class... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+using IdVec = std::vector<uint32_t, UninitAlloc<uint32_t>>;
+}  // namespace saba_cu
+
 struct saba_hgraph {
     uint32_t n = 0;
     uint64_t m = 0;
-    std::vector<uint32_t> off;  // n + 1 offsets (graph.hpp:242 layout)
-    std::vector<uint32_t> adj;  // 2m neighbour ids, ascending per slice
+    saba_cu::IdVec off;  // n + 1 offsets (graph.hpp:242 layout)
+    saba_cu::IdVec adj;  // 2m neighbour ids, ascending per slice
 };
 
 namespace saba_cu {

@@ -13,17 +13,34 @@ import numpy as np
 from . import _lib as L
 
 
+class _HostCsr:
+    """Owns a saba_hgraph handle; the numpy views of its CSR keep it alive
+    (no copy of the up-to-GB adjacency out of the library)."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if self.h:
+            L.lib().saba_hgraph_free(self.h)
+            self.h = None
+
+    def view(self, ptr, count):
+        if count == 0:
+            return np.zeros(0, np.uint32)
+        buf = (C.c_uint32 * count).from_address(C.addressof(ptr.contents))
+        buf._owner = self  # the ctypes buffer (the array's base) pins the handle
+        return np.frombuffer(buf, dtype=np.uint32)
+
+
 def _from_handle(h) -> "Graph":
     lib = L.lib()
-    try:
-        n = lib.saba_hgraph_vertex_count(h)
-        m = lib.saba_hgraph_edge_count(h)
-        off = np.zeros(n + 1, np.uint32)
-        adj = np.zeros(2 * m, np.uint32)
-        L.check(lib.saba_hgraph_csr(h, L.ptr(off, L.u32p), L.ptr(adj, L.u32p)), "csr")
-    finally:
-        lib.saba_hgraph_free(h)
-    return Graph(off, adj, _trusted=True)
+    owner = _HostCsr(h)
+    n = lib.saba_hgraph_vertex_count(h)
+    m = lib.saba_hgraph_edge_count(h)
+    po, pa = L.u32p(), L.u32p()
+    L.check(lib.saba_hgraph_data(h, C.byref(po), C.byref(pa)), "csr")
+    return Graph(owner.view(po, n + 1), owner.view(pa, 2 * m), _trusted=True)
 
 
 def _gen(fn, *args) -> "Graph":
