@@ -1456,7 +1456,7 @@ int saba_cu_truncated_lengths(saba_cu_graph* g, double epsilon, uint32_t power_i
         const HostCsr h{g->n, g->m, g->h_off.data(), host_adj(g).data()};
         DeviceSpmv dev{g};
         const SpmvFn spmv = dev.fn();
-        const Plan p = host_truncated_lengths(h, slot_edges(g), epsilon, power_iterations,
+        const Plan p = host_truncated_lengths(h, per_edge ? slot_edges(g).data() : nullptr, epsilon, power_iterations,
                                               max_truncation, per_edge != 0, &spmv);
         std::copy(p.tau.begin(), p.tau.end(), tau_out);
         *lambda_hat = p.lambda_hat;
@@ -1488,7 +1488,9 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
         const HostCsr h{g->n, g->m, g->h_off.data(), hadj.data()};
         check_data(host_is_connected(h), "aesc: spanning centrality requires a connected graph");
         lap("connectivity");
-        const auto& se = slot_edges(g);
+        // slot -> edge ids: only per-edge plans and the s_hat symmetrisation need them
+        const bool full = sources == nullptr && shard_count == 1;
+        const uint32_t* se = cfg->per_edge_tau || (full && s_hat_out) ? slot_edges(g).data() : nullptr;
         lap("slot edges");
         // aesc.hpp:649: the plan is built for epsilon / 2
         DeviceSpmv dev{g};
@@ -1647,11 +1649,10 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
             prop_ms[0] += prop_ms[w];
             walk_ms[0] += walk_ms[w];
         }
-        const bool full = sources == nullptr && shard_count == 1;
         if (full && s_hat_out) {
             double* d_s = static_cast<double*>(E0.st->s_hat.ensure(sizeof(double) * m));
             uint32_t* d_se = static_cast<uint32_t*>(E0.st->slot_edge_d.ensure(sizeof(uint32_t) * 2 * m));
-            SABA_CUDA_CHECK(cudaMemcpyAsync(d_se, se.data(), sizeof(uint32_t) * 2 * m, cudaMemcpyHostToDevice, E0.s));
+            copy_h2d(d_se, se, sizeof(uint32_t) * 2 * m, E0.s);
             aesc_symmetrise<<<g->sm_count * 4, 256, 0, E0.s>>>(g->d_csr, g->d_adj, d_se, n, d_g, d_s);
             SABA_CUDA_CHECK(cudaGetLastError());
             ++E0.launches;

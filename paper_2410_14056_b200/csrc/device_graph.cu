@@ -205,13 +205,11 @@ void pool_free(void* p) {
     cudaFreeAsync(p, 0);
 }
 
-const std::vector<uint32_t>& host_adj(saba_cu_graph* g) {
+const IdVec& host_adj(saba_cu_graph* g) {
     if (g->h_adj.size() != 2 * g->m) {
         DeviceScope scope(g->device);
-        g->h_adj.resize(2 * g->m);
-        if (g->m)
-            SABA_CUDA_CHECK(cudaMemcpy(g->h_adj.data(), g->d_adj, sizeof(uint32_t) * 2 * g->m,
-                                       cudaMemcpyDeviceToHost));
+        g->h_adj.resize(2 * g->m);  // not zero-filled: copy_d2h writes every slot
+        if (g->m) copy_d2h(g->h_adj.data(), g->d_adj, sizeof(uint32_t) * 2 * g->m, 0);
     }
     return g->h_adj;
 }
@@ -220,12 +218,12 @@ void set_last_error(const std::string& msg) { t_last_error = msg; }
 
 void release_aesc_state(saba_cu_graph* g);  // aesc.cu
 
-const std::vector<uint32_t>& slot_edges(saba_cu_graph* g) {
+const IdVec& slot_edges(saba_cu_graph* g) {
     if (!g->h_slot_edge.empty() || g->m == 0) return g->h_slot_edge;
     // edge ids are ranks of the (u<v) pairs in sorted order (graph.hpp:92-100)
     const auto& off = g->h_off;
     const auto& adj = host_adj(g);
-    std::vector<uint32_t> se(2 * g->m);
+    IdVec se(2 * g->m);  // every slot is written below
     // forward slots (u -> v, v > u) are numbered in CSR order: per-vertex
     // counts, a prefix sum, then independent numbering and reverse lookups
     const int64_t N = g->n;

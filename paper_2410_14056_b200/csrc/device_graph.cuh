@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "capi_util.hpp"
+#include "hgraph.hpp"
 
 namespace saba_cu {
 
@@ -71,8 +72,8 @@ struct saba_cu_graph {
     uint32_t max_degree = 0;
     uint32_t min_degree = 0;
     std::vector<uint32_t> h_off;         // host offsets (graph.hpp:242 layout)
-    std::vector<uint32_t> h_adj;         // host adjacency, fetched lazily (host_adj)
-    std::vector<uint32_t> h_slot_edge;   // directed slot -> edge id (lazy)
+    saba_cu::IdVec h_adj;                // host adjacency, fetched lazily (host_adj)
+    saba_cu::IdVec h_slot_edge;          // directed slot -> edge id (lazy)
     uint2* d_csr = nullptr;              // {base, degree} per vertex
     uint32_t* d_adj = nullptr;           // 2m neighbour ids, sorted per slice
     // 3 x 21-bit ids per uint64 when n <= 2^21 (2.67 B/slot instead of 4):
@@ -101,8 +102,8 @@ struct saba_cu_graph {
 };
 
 namespace saba_cu {
-const std::vector<uint32_t>& slot_edges(saba_cu_graph* g);
-const std::vector<uint32_t>& host_adj(saba_cu_graph* g);  // D2H once, then cached
+const IdVec& slot_edges(saba_cu_graph* g);
+const IdVec& host_adj(saba_cu_graph* g);  // D2H once, then cached
 // Build the fat adjacency once (false if {id, base, degree} exceed 64 bits).
 bool ensure_fat(saba_cu_graph* g);
 // Fat adjacency is worth it while it stays comfortably L2-resident.

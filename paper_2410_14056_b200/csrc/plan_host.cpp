@@ -178,7 +178,7 @@ uint32_t make_odd_clamped(double raw, uint32_t max_truncation, bool& clamped) {
 }
 }  // namespace
 
-Plan host_truncated_lengths(const HostCsr& g, const std::vector<uint32_t>& slot_edge, double eps,
+Plan host_truncated_lengths(const HostCsr& g, const uint32_t* slot_edge, double eps,
                             uint32_t omega, uint32_t max_truncation, bool per_edge, const SpmvFn* spmv) {
     check_arg(eps > 0.0 && eps < 1.0, "truncated_lengths: epsilon must be in (0,1)");
     check_arg(omega >= 1, "truncated_lengths: omega must be >= 1");

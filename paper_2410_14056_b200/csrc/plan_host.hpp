@@ -32,7 +32,7 @@ using SpmvFn = std::function<void(const std::vector<double>& x, const std::vecto
                                   std::vector<double>& y)>;
 double host_estimate_decay(const HostCsr& g, uint32_t iters, bool bip, const std::vector<char>& side,
                            const SpmvFn* spmv = nullptr);
-Plan host_truncated_lengths(const HostCsr& g, const std::vector<uint32_t>& slot_edge, double eps,
+Plan host_truncated_lengths(const HostCsr& g, const uint32_t* slot_edge, double eps,
                             uint32_t omega, uint32_t max_truncation, bool per_edge,
                             const SpmvFn* spmv = nullptr);
 double walks_needed_raw(int64_t tau_eff, double eps, double delta, uint32_t degree, uint64_t m);
