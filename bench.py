@@ -24,7 +24,6 @@ import json
 import os
 import statistics
 import sys
-import time
 
 import numpy as np
 
@@ -265,7 +264,10 @@ def run_ours(args):
     for i in range(args.warmup + args.steps):
         if world > 1:
             dist.barrier()
-        t0 = time.perf_counter()
+        # device events bracket the whole blocking API call (H2D, walks, D2H)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
         sink = sb.VisitCountSink(g.n)
         sb.run_walk_campaign(ge, cfg, sink, total_walks=total_walks, shard_index=rank,
                              shard_count=world, device=local)
@@ -274,9 +276,10 @@ def run_ours(args):
             dist.all_reduce(ct)
             host_counts.copy_(ct)
         ge.release_device()
-        t1 = time.perf_counter()
+        e1.record(stream)
+        e1.synchronize()
         if i >= args.warmup:
-            e2e_t.append(t1 - t0)
+            e2e_t.append(e0.elapsed_time(e1) * 1e-3)
     e2e_tot = torch.tensor([sum(e2e_t)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
@@ -328,13 +331,19 @@ def aesc_cfg3_summary(sb, args):
     source), 1 warm-up + 1 timed run, with the reference's own CPU path timed
     on a 64-source sample and extrapolated (bench.py --workload cfg3 is the
     full-protocol measurement)."""
+    import torch
     spec, eps, delta, _, cpu_sources = AESC_WORKLOADS["cfg3"]
     g = make_aesc_graph(sb, spec)
     cfg = sb.AescConfig(epsilon=eps, delta=delta)
     sb.aesc(g, cfg)  # warm-up
-    t0 = time.perf_counter()
+    stream = torch.cuda.current_stream(0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(0)
+    e0.record(stream)
     est = sb.aesc(g, cfg)
-    wall = time.perf_counter() - t0
+    e1.record(stream)
+    e1.synchronize()
+    wall = e0.elapsed_time(e1) * 1e-3
     res = {"workload": f"cfg3: R-MAT s16 ef8 LCC n={g.n} m={g.m} eps={eps} delta={delta}, all sources",
            "seconds": wall, "unit": "s", "higher_is_better": False,
            "walk_pairs": est.total_walk_pairs, "walk_steps": est.total_walk_steps,
@@ -434,15 +443,23 @@ def run_aesc_bench(args):
         label = f"all {g.n} sources"
     g.device_handle(local)
 
+    stream = torch.cuda.current_stream(local)
+
     def one(graph):
-        t0 = time.perf_counter()
+        # CUDA events on the current stream bracket the whole (blocking) call,
+        # host planning included: the device-timeline span of one AESC run
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(local)
+        e0.record(stream)
         est = sb.aesc(graph, cfg, sources=sources, shard_index=rank, shard_count=world, device=local)
         gh = est.g_hat
         if world > 1:
             t = torch.from_numpy(gh).to(f"cuda:{local}")
             dist.all_reduce(t)  # each slot has one writer: the sum is exact
             gh = t.cpu().numpy()
-        return time.perf_counter() - t0, est, gh
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) * 1e-3, est, gh
 
     for _ in range(args.warmup):
         one(g)
@@ -471,10 +488,14 @@ def run_aesc_bench(args):
     ge = sb.Graph(pin_off, pin_adj, _trusted=True)
     e2e = []
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        dt, _, _ = one(ge)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(local)
+        e0.record(stream)
+        one(ge)
         ge.release_device()
-        e2e.append(time.perf_counter() - t0)
+        e1.record(stream)
+        e1.synchronize()
+        e2e.append(e0.elapsed_time(e1) * 1e-3)
     e2e_t = torch.tensor([sum(e2e)], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)

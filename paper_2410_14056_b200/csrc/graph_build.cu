@@ -203,6 +203,7 @@ struct Timer {
 // purpose, all from the stream-ordered pool. Buffers are never resized
 // mid-pipeline (the pool frees on the legacy stream, not on `s`).
 struct Builder {
+    DeviceScope scope;  // the caller's current device is restored on return
     cudaStream_t s = nullptr;
     int grid = 148 * 8;
     DevBuf k0, k1, tmp, num, in_pairs, in_max, parent, comp, size, skey, flag, relab, off, gen_a, gen_b;
@@ -210,8 +211,7 @@ struct Builder {
     uint64_t samples = 0;
     uint64_t* dir() { return scratch<uint64_t>(k0, 2 * samples); }
 
-    explicit Builder(int device) {
-        SABA_CUDA_CHECK(cudaSetDevice(device));
+    explicit Builder(int device) : scope(device) {
         ensure_pool(device);
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
