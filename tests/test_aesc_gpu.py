@@ -199,6 +199,33 @@ def test_rmat_full_aesc_matches_oracle(sb, oracle):
     assert close(est.s_hat, ref.s_hat)
 
 
+def test_hub_rows_every_path_matches_oracle(sb, oracle):
+    """Rows above the 256-neighbour piece threshold on every propagation path:
+    a graph of hub rows only (a ring of eight K_258: every degree >= 257, so
+    dense depths have no light-row work list and the pieces kernel takes every
+    hub row), and hubs joined by light rows (sparse depths list the heavy
+    candidates, dense depths hand pieces out with the light rows)."""
+    k, c = 258, 8
+    pairs = []
+    for q in range(c):
+        b = q * k
+        pairs += [(b + u, b + v) for u in range(k) for v in range(u + 1, k)]
+        pairs.append((b + k - 1, ((q + 1) % c) * k))
+    hubs = sb.Graph.from_edges(k * c, pairs)
+    assert int(np.diff(hubs.offsets).min()) > 256
+    rng = np.random.default_rng(11)
+    spokes = [(h, int(x)) for h in range(4) for x in rng.choice(np.arange(4, 3000), 400, replace=False)]
+    mixed = sb.Graph.from_edges(3000, spokes + [(v, v + 1) for v in range(3, 2999)])
+    for g, eps in ((hubs, 0.2), (mixed, 0.1)):
+        assert g.max_degree() > 256
+        src = np.arange(0, g.n, max(1, g.n // (8 if g is hubs else 96)), dtype=np.uint32)
+        est = sb.aesc(g, sb.AescConfig(epsilon=eps, delta=0.05), sources=src)
+        ref = oracle.aesc(g.offsets, g.adjacency, epsilon=eps, delta=0.05, sources=src)
+        assert np.array_equal(est.plan.tau_tilde[src], ref.tau_tilde[src])
+        assert est.total_walk_pairs == ref.total_walk_pairs
+        assert close(est.g_hat, ref.g_hat), worst(est.g_hat, ref.g_hat)
+
+
 def test_source_subset_and_shards(sb, oracle):
     g = sb.make_rmat(12, 8, seed=5)
     src = np.array([0, 1, 2, 7, 100, 513, g.n - 1], np.uint32)
