@@ -764,7 +764,7 @@ __global__ void __launch_bounds__(256)
 // WPT walks per lane, MINB resident blocks per SM (register budget): short
 // walks are prologue/latency bound and want many warps with 2 walks each
 // (32 registers), long ones 4 walks per lane (48 registers); see run_tiles.
-template <bool PACKED, int WPT, bool BITMAP, bool FAT, int MINB>
+template <bool PACKED, int WPT, bool BITMAP, bool FAT, int MINB, bool F16 = false>
 __global__ void __launch_bounds__(256, MINB)
     aesc_walk_sorted(const uint32_t* __restrict__ gidx, const uint32_t* __restrict__ vals,
                      uint32_t nwalks, const WalkGroup* __restrict__ groups,
@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(256, MINB)
                      const uint64_t* __restrict__ adjp, const double* __restrict__ R, uint32_t n,
                      const uint32_t* __restrict__ bits, uint32_t words, uint64_t mult,
                      const uint64_t* __restrict__ fat, uint32_t fat_idb, uint32_t fat_sh,
-                     double* __restrict__ score) {
+                     const uint4* __restrict__ fat16, double* __restrict__ score) {
     // Software-pipelined score side: the walk chain (csr -> adj, or one fat
     // gather) is the only dependency carried from step to step; the support
     // bit of x_l is loaded right after x_l is known, the rho gather of x_l is
@@ -812,12 +812,12 @@ __global__ void __launch_bounds__(256, MINB)
         }
         maxlen = __reduce_max_sync(0xffffffffu, maxlen);
         uint2 rec[WPT];
-        if constexpr (FAT) {
+        if constexpr (FAT || F16) {
 #pragma unroll
             for (int r = 0; r < WPT; ++r) rec[r] = len[r] > 1 ? ldg_csr(csr + cur[r]) : make_uint2(0, 1);
         }
         for (uint32_t l = 1; l < maxlen + 2; ++l) {
-            if constexpr (!FAT) {  // critical load of step l first
+            if constexpr (!FAT && !F16) {  // critical load of step l first
 #pragma unroll
                 for (int r = 0; r < WPT; ++r)
                     if (l < len[r]) rec[r] = ldg_csr(csr + cur[r]);
@@ -833,7 +833,11 @@ __global__ void __launch_bounds__(256, MINB)
             for (int r = 0; r < WPT; ++r)
                 if (l < len[r]) {
                     const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
-                    if constexpr (FAT) {
+                    if constexpr (F16) {
+                        const uint4 f = __ldg(fat16 + (rec[r].x + scaled_index(raw, rec[r].y)));
+                        cur[r] = f.x;
+                        rec[r] = make_uint2(f.y, f.z);
+                    } else if constexpr (FAT) {
                         const uint64_t f = __ldg(reinterpret_cast<const unsigned long long*>(fat) + rec[r].x +
                                                  scaled_index(raw, rec[r].y));
                         cur[r] = uint32_t(f & idmask);
@@ -1213,6 +1217,19 @@ struct TileBuilder {
 
 // Walk phase: per chunk keygen -> radix sort (group, seed top bits) -> sorted
 // walks -> pair tiles; then the per-slot fold into g_hat.
+// Short walks beyond L2 (plan max tau below kShortWalk) step through 16-byte
+// {id, base, degree} records: one dependent gather per step instead of csr
+// then adjacency. Measured: cfg5 (tau 15) walks 4% faster; cfg4 (tau 127,
+// long walks) 12% slower, as the 4x footprint costs L2 hits on hub lists.
+// SABA_AESC_FAT16=0 disables.
+constexpr uint32_t kShortWalk = 20;
+bool aesc_fat16_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SABA_AESC_FAT16");
+        return !e || atoi(e) != 0;
+    }();
+    return on;
+}
 bool aesc_fat_enabled() {  // SABA_AESC_FAT=0 disables (default: on when L2-resident)
     static const bool on = [] {
         const char* e = getenv("SABA_AESC_FAT");
@@ -1303,22 +1320,24 @@ struct Launch {
     cudaStream_t s;
 };
 
-template <bool P, int WPT, bool B, bool F, int MINB>
+template <bool P, int WPT, bool B, bool F, int MINB, bool F16 = false>
 void walk_launch(const Launch& L) {
-    auto k = aesc_walk_sorted<P, WPT, B, F, MINB>;
+    auto k = aesc_walk_sorted<P, WPT, B, F, MINB, F16>;
     int occ = 0;
     SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0));
     const int grid = int(std::min<uint64_t>((uint64_t(L.nw) + 32 * WPT - 1) / (32 * WPT) * 32 / 256 + 1,
                                             uint64_t(L.g->sm_count) * std::max(occ, 1)));
     k<<<grid, 256, 0, L.s>>>(L.out_g, L.out_w, L.nw, L.dg, L.g->d_csr, L.g->d_adj, L.g->d_adj_packed, L.R,
                              L.g->n, L.bits, L.words, L.mult, L.g->d_adj_fat, L.g->fat_idb, L.g->fat_sh,
-                             L.score);
+                             L.g->d_adj_fat16, L.score);
 }
 
 template <int WPT, int MINB>
-void walk_dispatch(const Launch& L, bool fat, bool packed) {
+void walk_dispatch(const Launch& L, bool fat, bool packed, bool f16) {
     const bool b = L.bits != nullptr;
-    if (fat) {
+    if (f16) {
+        if (b) walk_launch<false, WPT, true, false, MINB, true>(L); else walk_launch<false, WPT, false, false, MINB, true>(L);
+    } else if (fat) {
         if (b) walk_launch<false, WPT, true, true, MINB>(L); else walk_launch<false, WPT, false, true, MINB>(L);
     } else if (packed) {
         if (b) walk_launch<true, WPT, true, false, MINB>(L); else walk_launch<true, WPT, false, false, MINB>(L);
@@ -1335,6 +1354,7 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
     const bool packed = g->d_adj_packed != nullptr;
     // the fat adjacency is built (main thread) before any batch worker runs
     const bool fat = g->d_adj_fat != nullptr && fat_fits_l2(g) && aesc_fat_enabled();
+    const bool f16 = !fat && g->d_adj_fat16 != nullptr && aesc_fat16_enabled();  // built for short plans only
     SortScratch scratch;
     for (TileBuilder::Chunk& c : tb.chunks) {
         const uint32_t ng = uint32_t(c.groups.size()), nw = c.walks, nt = uint32_t(c.tiles.size());
@@ -1349,12 +1369,12 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         // walk shape of the chunk: mean steps per walk decides the variant
         // (measured: cfg5, ~12 steps, 2 x 8 beats 4 x 5 by 12%; cfg3/cfg4,
         // 24-73 steps, 4 x 5 is best by 3-4%)
-        const bool short_walks = c.steps < 20ull * nw;
+        const bool short_walks = c.steps < uint64_t(kShortWalk) * nw;
         const Launch L{out_g, out_w, nw, dg, g, R, bits, words, mult, score, s};
         if (short_walks)
-            walk_dispatch<2, 8>(L, fat, packed);
+            walk_dispatch<2, 8>(L, fat, packed, f16);
         else
-            walk_dispatch<4, 5>(L, fat, packed);
+            walk_dispatch<4, 5>(L, fat, packed, false);
         SABA_CUDA_CHECK(cudaGetLastError());
         aesc_pair_reduce<<<int(std::min<uint32_t>(nt, g->sm_count * 8)), 256, 0, s>>>(dt, nt, dg, score, part);
         SABA_CUDA_CHECK(cudaGetLastError());
@@ -1502,7 +1522,10 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
         const uint32_t n = g->n;
         const uint64_t m = g->m;
         for (uint64_t i = 0; i < source_count; ++i) check_arg(sources[i] < n, "source out of range");
-        if (fat_fits_l2(g) && aesc_fat_enabled()) ensure_fat(g);  // before the workers start
+        if (fat_fits_l2(g) && aesc_fat_enabled())
+            ensure_fat(g);  // before the workers start
+        else if (plan.max_tau < kShortWalk && aesc_fat16_enabled())
+            ensure_fat16(g);
         lap("fat adjacency");
         Engine E(g);
         lap("engine");

@@ -54,7 +54,27 @@ __global__ void build_fat_kernel(const uint2* __restrict__ csr, const uint32_t* 
         fat[s] = uint64_t(v) | (uint64_t(r.x) << idb) | (uint64_t(r.y) << sh);
     }
 }
+__global__ void build_fat16_kernel(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                                   uint64_t two_m, uint4* __restrict__ fat16) {
+    for (uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < two_m;
+         s += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t v = adj[s];
+        const uint2 r = csr[v];
+        fat16[s] = make_uint4(v, r.x, r.y, 0u);
+    }
+}
 }  // namespace
+
+bool ensure_fat16(saba_cu_graph* g) {
+    if (g->fat16_tried) return g->d_adj_fat16 != nullptr;
+    g->fat16_tried = true;
+    if (g->m == 0) return false;
+    g->d_adj_fat16 = static_cast<uint4*>(pool_alloc(sizeof(uint4) * 2 * g->m));
+    build_fat16_kernel<<<g->sm_count * 8, 256>>>(g->d_csr, g->d_adj, 2 * g->m, g->d_adj_fat16);
+    SABA_CUDA_CHECK(cudaGetLastError());
+    SABA_CUDA_CHECK(cudaDeviceSynchronize());
+    return true;
+}
 
 bool ensure_fat(saba_cu_graph* g) {
     if (g->fat_tried) return g->d_adj_fat != nullptr;
@@ -267,6 +287,7 @@ saba_cu_graph::~saba_cu_graph() {
     if (d_adj) saba_cu::pool_free(d_adj);
     if (d_adj_packed) saba_cu::pool_free(d_adj_packed);
     if (d_adj_fat) saba_cu::pool_free(d_adj_fat);
+    if (d_adj_fat16) saba_cu::pool_free(d_adj_fat16);
     if (d_csr_hot) saba_cu::pool_free(d_csr_hot);
     if (d_hot_vertex) saba_cu::pool_free(d_hot_vertex);
     if (ev0) cudaEventDestroy(ev0);

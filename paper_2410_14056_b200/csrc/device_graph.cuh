@@ -84,6 +84,10 @@ struct saba_cu_graph {
     // so a walk step is one dependent gather instead of two. Built on first
     // use when the three fields fit in 64 bits.
     uint64_t* d_adj_fat = nullptr;
+    // 16-byte records {id, base, degree, 0} per slot (AESC walks on graphs
+    // too large for the 8-byte fat form): one dependent gather per step
+    uint4* d_adj_fat16 = nullptr;
+    bool fat16_tried = false;
     uint32_t fat_idb = 0, fat_sh = 0;
     bool fat_tried = false;
     // Hub-privatised counting: {base, degree | (hot slot + 1) << hot_shift};
@@ -106,6 +110,7 @@ const IdVec& slot_edges(saba_cu_graph* g);
 const IdVec& host_adj(saba_cu_graph* g);  // D2H once, then cached
 // Build the fat adjacency once (false if {id, base, degree} exceed 64 bits).
 bool ensure_fat(saba_cu_graph* g);
+bool ensure_fat16(saba_cu_graph* g);
 // Fat adjacency is worth it while it stays comfortably L2-resident.
 inline bool fat_fits_l2(const saba_cu_graph* g) { return 16 * g->m <= (uint64_t(48) << 20); }
 constexpr uint32_t kPackBits = 21;
