@@ -84,10 +84,12 @@ struct AescState {
     DevBuf light_order;  // light rows by descending degree (dense depths)
     uint32_t nlight = 0;
     bool heavy_built = false;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;       // propagation (and everything else)
+    cudaStream_t stream_walk = nullptr;  // walk phase of the batch workers
     uint64_t* h_ctrl = nullptr;  // pinned mirror of the control block
     ~AescState() {
         if (stream) cudaStreamDestroy(stream);
+        if (stream_walk) cudaStreamDestroy(stream_walk);
         if (h_ctrl) cudaFreeHost(h_ctrl);
     }
 };
@@ -942,7 +944,16 @@ struct Engine {
         if (!g->aesc) g->aesc = new AescState[kWorkspaces];
         st = &g->aesc[workspace];
         if (!st->stream) {
-            SABA_CUDA_CHECK(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+            // two batches in flight contend for the SMs: the propagation is a
+            // serial chain of short kernels, the walk phase a few long ones,
+            // so propagation runs on a high-priority stream and the walks on
+            // a low-priority one (SABA_AESC_PRIO=0: one default stream)
+            int lo = 0, hi = 0;
+            SABA_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            const char* e = getenv("SABA_AESC_PRIO");
+            if (e && atoi(e) == 0) lo = hi = 0;
+            SABA_CUDA_CHECK(cudaStreamCreateWithPriority(&st->stream, cudaStreamNonBlocking, hi));
+            SABA_CUDA_CHECK(cudaStreamCreateWithPriority(&st->stream_walk, cudaStreamNonBlocking, lo));
             SABA_CUDA_CHECK(cudaHostAlloc(&st->h_ctrl, sizeof(uint64_t) * kCtrlWords, cudaHostAllocDefault));
         }
         s = st->stream;
@@ -1629,7 +1640,10 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
                     const uint32_t tt_max = *std::max_element(tt.begin(), tt.end());
                     const bool use_bits = bitmap_mode == 1 || (bitmap_mode == 2 && tt_max <= 4);
                     const auto h2 = std::chrono::steady_clock::now();
-                    run_tiles(g, W.st, W.s, tb, W.st->R.as<double>(),
+                    // the propagation above ended with a host sync, and run_tiles
+                    // returns after its own, so the two streams never overlap
+                    // within one worker
+                    run_tiles(g, W.st, W.st->stream_walk, tb, W.st->R.as<double>(),
                               use_bits ? W.st->bits.as<uint32_t>() : nullptr, cfg->hash_multiplier,
                               d_g, &W.launches);
                     SABA_CUDA_CHECK(cudaEventRecord(e2, W.s));
