@@ -19,10 +19,11 @@ class _HostCsr:
 
     def __init__(self, h):
         self.h = h
+        self._free = L.lib().saba_hgraph_free  # bound now: usable during interpreter shutdown
 
     def __del__(self):
         if self.h:
-            L.lib().saba_hgraph_free(self.h)
+            self._free(self.h)
             self.h = None
 
     def view(self, ptr, count):
