@@ -1352,6 +1352,7 @@ void walk_dispatch(const Launch& L, bool fat, bool packed, bool f16) {
         if (b) walk_launch<false, WPT, true, true, MINB>(L); else walk_launch<false, WPT, false, true, MINB>(L);
     } else if (packed) {
         if (b) walk_launch<true, WPT, true, false, MINB>(L); else walk_launch<true, WPT, false, false, MINB>(L);
+
     } else {
         if (b) walk_launch<false, WPT, true, false, MINB>(L); else walk_launch<false, WPT, false, false, MINB>(L);
     }
@@ -1570,14 +1571,13 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
         // Batches alternate between kWorkspaces workers, each with its own
         // buffers, stream and host thread, so one batch's propagation
         // overlaps another's walk phase. Sources write disjoint g_hat slots.
-        // A second worker pays off only when propagation is deep enough to
-        // overlap with walks; shallow plans are walk-bound and two walk
-        // phases would only contend for DRAM.
         static const int workers_env = [] {  // SABA_AESC_WORKERS=1|2 overrides
             const char* e = getenv("SABA_AESC_WORKERS");
             return e ? std::max(1, std::min(kWorkspaces, atoi(e))) : 0;
         }();
-        const int nworkers = workers_env ? workers_env : (plan.max_tau > 31 ? kWorkspaces : 1);
+        // (measured: 3 workers gain nothing on cfg3/cfg4; 2 beat 1 on cfg3 and,
+        // since the walk phase got cheaper, on the shallow cfg5 plan too: -11%)
+        const int nworkers = workers_env ? workers_env : (list.size() > size_t(kCols) ? kWorkspaces : 1);
         std::vector<std::unique_ptr<Engine>> engines;
         engines.emplace_back(new Engine(std::move(E)));
         for (int w = 1; w < nworkers; ++w) {
