@@ -1352,7 +1352,6 @@ void walk_dispatch(const Launch& L, bool fat, bool packed, bool f16) {
         if (b) walk_launch<false, WPT, true, true, MINB>(L); else walk_launch<false, WPT, false, true, MINB>(L);
     } else if (packed) {
         if (b) walk_launch<true, WPT, true, false, MINB>(L); else walk_launch<true, WPT, false, false, MINB>(L);
-
     } else {
         if (b) walk_launch<false, WPT, true, false, MINB>(L); else walk_launch<false, WPT, false, false, MINB>(L);
     }
