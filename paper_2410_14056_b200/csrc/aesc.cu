@@ -16,11 +16,14 @@
 //                      support masks (support(l+1) = N(support(l)),
 //                      aesc.hpp:313-325) and the exact support degree sums
 //   K3f aesc_hook      g_hat[s] += p_l(i)/d_i - p_l(j)/d_j (aesc.hpp:581-588)
-//   K4  aesc_walk      two-way walk pairs (aesc.hpp:448-525): a block owns a
-//                      tile of 2048 pair indices, sorts each side's seeds in
-//                      shared memory (a SABA bouquet per warp, PAPER Alg. 3),
-//                      walks them scoring rho in step order, and reduces
-//                      (a_k - b_k) / n_req with a fixed tree
+//   K4s sort_coarse_count / sort_coarse_scatter / sort_fine
+//                      SABA bucketing of each (slot, side) seed set by its top
+//                      seed bits, ~32 walks per bucket (PAPER Alg. 3), as a
+//                      segment-local counting sort
+//   K4  aesc_walk_sorted two-way walk pairs (aesc.hpp:448-525): warps walk 32
+//                      adjacent seeds of one (slot, side), scoring rho in
+//                      step order; aesc_pair_reduce folds (a_k - b_k) / n_req
+//                      per 2048-pair tile with a fixed tree
 //   K4b aesc_slot_reduce  per directed slot: tile partials folded in tile
 //                      order, g_hat[s] += acc (aesc.hpp:624)
 //   K5  aesc_symmetrise s_hat[e] = g_hat[u->v] + g_hat[v->u] (aesc.hpp:702-706)
@@ -1181,12 +1184,6 @@ void validate_cfg(const saba_cu_aesc_config& c) {
 }
 
 // Host plan of one walk phase: slots -> groups -> chunks, tiles in pair order.
-int bits_for(uint32_t x) {
-    int b = 0;
-    while ((1ull << b) < x) ++b;
-    return b;
-}
-
 struct TileBuilder {
     struct Chunk {
         std::vector<WalkGroup> groups;
