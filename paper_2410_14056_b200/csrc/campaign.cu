@@ -9,7 +9,12 @@
 //                           (walker.hpp:439) -> a warp is a 32-lane bouquet
 //   K2  walk_count_kernel   L-1 lockstep hashed steps per lane
 //                           (walker.hpp:221-235) + VisitCountSink epilogue
-//                           (walker.hpp:355) as warp-aggregated L2 reductions
+//                           (walker.hpp:355) as warp-aggregated L2 reductions;
+//                           the default walk_count_hot_kernel counts visits at
+//                           departure and keeps the ~32K highest-degree
+//                           vertices' counters in shared memory (one
+//                           1024-thread block per SM), walk_count_fat_kernel
+//                           takes one gather per step on L2-resident graphs
 //
 // A GPU bouquet is a warp: lanes hold consecutive entries of the sorted key
 // array, so they share their start vertex and hold adjacent seeds — the
