@@ -1231,6 +1231,13 @@ struct TileBuilder {
 // long walks) 12% slower, as the 4x footprint costs L2 hits on hub lists.
 // SABA_AESC_FAT16=0 disables.
 constexpr uint32_t kShortWalk = 20;
+#ifndef SABA_SHORT_WPT
+#define SABA_SHORT_WPT 1
+#endif
+#ifndef SABA_SHORT_MINB
+#define SABA_SHORT_MINB 8
+#endif
+constexpr int kShortWpt = SABA_SHORT_WPT, kShortMinb = SABA_SHORT_MINB;  // short-walk variant
 bool aesc_fat16_enabled() {
     static const bool on = [] {
         const char* e = getenv("SABA_AESC_FAT16");
@@ -1375,12 +1382,13 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         double* score = static_cast<double*>(st->score.ensure(sizeof(double) * nw));
         bucket_walks(st, s, c, dg, scratch, out_w, out_g, launches);
         // walk shape of the chunk: mean steps per walk decides the variant
-        // (measured: cfg5, ~12 steps, 2 x 8 beats 4 x 5 by 12%; cfg3/cfg4,
-        // 24-73 steps, 4 x 5 is best by 3-4%)
+        // (measured on cfg5, ~12 steps, two workers: 1 walk/lane x 8 blocks
+        // 1.53 s, 2 x 8 1.63, 2 x 6 1.62, 3 x 6 1.80, 4 x 5 1.88 per 768
+        // sources; cfg3/cfg4, 24-73 steps: 4 x 5 is best by 3-4%)
         const bool short_walks = c.steps < uint64_t(kShortWalk) * nw;
         const Launch L{out_g, out_w, nw, dg, g, R, bits, words, mult, score, s};
         if (short_walks)
-            walk_dispatch<2, 8>(L, fat, packed, f16);
+            walk_dispatch<kShortWpt, kShortMinb>(L, fat, packed, f16);
         else
             walk_dispatch<4, 5>(L, fat, packed, false);
         SABA_CUDA_CHECK(cudaGetLastError());
