@@ -1385,7 +1385,11 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         // (measured on cfg5, ~12 steps, two workers: 1 walk/lane x 8 blocks
         // 1.53 s, 2 x 8 1.63, 2 x 6 1.62, 3 x 6 1.80, 4 x 5 1.88 per 768
         // sources; cfg3/cfg4, 24-73 steps: 4 x 5 is best by 3-4%)
-        const bool short_walks = c.steps < uint64_t(kShortWalk) * nw;
+        static const uint64_t short_steps = [] {  // SABA_SHORT_STEPS overrides (tuning knob)
+            const char* e = getenv("SABA_SHORT_STEPS");
+            return e ? uint64_t(atoi(e)) : uint64_t(kShortWalk);
+        }();
+        const bool short_walks = c.steps < short_steps * nw;
         const Launch L{out_g, out_w, nw, dg, g, R, bits, words, mult, score, s};
         if (short_walks)
             walk_dispatch<kShortWpt, kShortMinb>(L, fat, packed, f16);
