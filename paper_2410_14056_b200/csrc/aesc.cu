@@ -9,8 +9,9 @@
 //                      reference's repeated-addition budget (exact fallback
 //                      whenever the fast bound cannot decide), freezing
 //                      the source at tau~ = l
-//   K3c aesc_rho       rho = p_tau~ * inv_deg for frozen sources (aesc.hpp:597-602)
-//   K3d aesc_expand    sparse frontier: candidate rows of depth l+1
+//   K3c/d aesc_rho_expand  rho = p_tau~ * inv_deg for the sources frozen at
+//                      this depth (aesc.hpp:597-602), then the sparse frontier
+//                      growth: candidate rows of depth l+1
 //   K3e aesc_pull      p_{l+1}(x) = sum_{v in N(x)} p_l(v)/d(v) for all 64
 //                      columns at once (row = 512 B, lane = 2 columns), the
 //                      support masks (support(l+1) = N(support(l)),
@@ -238,10 +239,10 @@ __global__ void aesc_check(uint32_t* __restrict__ ucount_next, const uint32_t* _
 
 // rho for the columns frozen at this depth; rows outside the support hold
 // exact zeros in P and therefore in R.
-__global__ void aesc_rho(const double* __restrict__ P, const uint2* __restrict__ csr,
-                         const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
-                         const unsigned long long* __restrict__ ctrl, uint32_t n,
-                         double* __restrict__ R, uint32_t* __restrict__ bits, uint32_t words) {
+__device__ __forceinline__ void rho_body(const double* __restrict__ P, const uint2* __restrict__ csr,
+                                         const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
+                                         const unsigned long long* __restrict__ ctrl, uint32_t n,
+                                         double* __restrict__ R, uint32_t* __restrict__ bits, uint32_t words) {
     const unsigned long long fz = ctrl[kFrozenNow];
     if (!fz) return;
     const bool dense = ctrl[kDense] != 0;
@@ -275,13 +276,13 @@ __device__ __forceinline__ void warp_append(uint32_t* __restrict__ list, uint32_
 // Sparse frontier growth: rows of depth l+1 = N(rows of depth l that still
 // carry an active column). Warp per row; the order of the new list is
 // irrelevant (every row is computed independently).
-__global__ void aesc_expand(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
-                            const unsigned long long* __restrict__ M,
-                            const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
-                            uint32_t* __restrict__ ulist_next, uint32_t* __restrict__ ucount_next,
-                            uint32_t* __restrict__ flag, uint32_t* __restrict__ tflag,
-                            uint32_t* __restrict__ tlist, uint32_t* __restrict__ tcount,
-                            const unsigned long long* __restrict__ ctrl) {
+__device__ __forceinline__ void expand_body(const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                                            const unsigned long long* __restrict__ M,
+                                            const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
+                                            uint32_t* __restrict__ ulist_next, uint32_t* __restrict__ ucount_next,
+                                            uint32_t* __restrict__ flag, uint32_t* __restrict__ tflag,
+                                            uint32_t* __restrict__ tlist, uint32_t* __restrict__ tcount,
+                                            const unsigned long long* __restrict__ ctrl) {
     const unsigned long long active = ctrl[kActive];
     if (!active || ctrl[kDense]) return;
     const uint32_t lane = threadIdx.x & 31;
@@ -310,6 +311,21 @@ __global__ void aesc_expand(const uint2* __restrict__ csr, const uint32_t* __res
             warp_append(tlist, tcount, x, fresh, lane);
         }
     }
+}
+
+// K3c + K3d in one launch (one fewer kernel per depth): rho of the columns
+// frozen at this depth (reads P_l) and the sparse frontier growth (reads the
+// support masks) touch disjoint data, so one grid does both in turn.
+__global__ void aesc_rho_expand(const double* __restrict__ P, const uint2* __restrict__ csr,
+                                const uint32_t* __restrict__ adj, const unsigned long long* __restrict__ M,
+                                const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
+                                uint32_t* __restrict__ ulist_next, uint32_t* __restrict__ ucount_next,
+                                uint32_t* __restrict__ flag, uint32_t* __restrict__ tflag,
+                                uint32_t* __restrict__ tlist, uint32_t* __restrict__ tcount,
+                                const unsigned long long* __restrict__ ctrl, uint32_t n, double* __restrict__ R,
+                                uint32_t* __restrict__ bits, uint32_t words) {
+    rho_body(P, csr, ulist, ucount, ctrl, n, R, bits, words);
+    expand_body(csr, adj, M, ulist, ucount, ulist_next, ucount_next, flag, tflag, tlist, tcount, ctrl);
 }
 
 // Rows with more than kHeavy neighbours are split into fixed pieces of
@@ -1097,10 +1113,9 @@ struct Engine {
             aesc_check<<<1, kCols, 0, s>>>(UC + (cur ^ 1), st->col_src.as<uint32_t>(),
                                            st->col_tau.as<uint32_t>(), csr, tsl, p, DS[cur], DS[cur ^ 1],
                                            ttd, ctrl);
-            aesc_rho<<<grid, 256, 0, s>>>(P[cur], csr, UL[cur], UC + cur, ctrl, n, st->R.as<double>(),
-                                          st->bits.as<uint32_t>(), words());
-            aesc_expand<<<grid, 256, 0, s>>>(csr, adj, M[cur], UL[cur], UC + cur, UL[cur ^ 1],
-                                             UC + (cur ^ 1), flag, tflag, tlist, tcount, ctrl);
+            aesc_rho_expand<<<grid, 256, 0, s>>>(P[cur], csr, adj, M[cur], UL[cur], UC + cur, UL[cur ^ 1],
+                                                 UC + (cur ^ 1), flag, tflag, tlist, tcount, ctrl, n,
+                                                 st->R.as<double>(), st->bits.as<uint32_t>(), words());
             // sparse depths: pieces of candidate hub rows; dense depths: the
             // pull kernel takes the pieces into its dynamic work list
             if (st->npieces)
@@ -1121,7 +1136,7 @@ struct Engine {
             aesc_hook<<<kCols, 128, 0, s>>>(st->col_src.as<uint32_t>(), csr, adj, tsl, P[cur ^ 1], ctrl,
                                             g_hat_dev);
         };
-        const uint32_t per_depth = st->npieces ? 7 : 5;
+        const uint32_t per_depth = st->npieces ? 6 : 4;
         if (!depth_graph) {
             // depths_per_graph() depths (even, so the buffer parity returns to 0)
             // captured once per estimator call and replayed for every batch
