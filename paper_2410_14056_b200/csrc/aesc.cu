@@ -16,7 +16,8 @@
 //                      columns at once (row = 512 B, lane = 2 columns), the
 //                      support masks (support(l+1) = N(support(l)),
 //                      aesc.hpp:313-325) and the exact support degree sums
-//   K3f aesc_hook      g_hat[s] += p_l(i)/d_i - p_l(j)/d_j (aesc.hpp:581-588)
+//   K3f aesc_hook_check g_hat[s] += p_l(i)/d_i - p_l(j)/d_j (aesc.hpp:581-588),
+//                      fused with K3b of the next depth (block per column)
 //   K4s sort_coarse_count / sort_coarse_scatter / sort_fine
 //                      SABA bucketing of each (slot, side) seed set by its top
 //                      seed bits, ~32 walks per bucket (PAPER Alg. 3), as a
@@ -116,7 +117,8 @@ void release_aesc_state(saba_cu_graph* g) {
 namespace {
 
 // Control block (device): active mask, frozen-at-this-depth mask, dense flag.
-enum { kActive = 0, kFrozenNow = 1, kDense = 2, kDenseReq = 3, kDepth = 4, kRowNext = 5, kCtrlWords = 8 };
+enum { kActive = 0, kFrozenNow = 1, kDense = 2, kDenseReq = 3, kDepth = 4, kRowNext = 5, kFrozenAcc = 6,
+       kDone = 7, kCtrlWords = 8 };
 
 struct AescParams {
     double eps, delta, log_term;  // log_term = log(4m/delta) (aesc.hpp:109)
@@ -196,6 +198,8 @@ __global__ void aesc_init(const uint32_t* __restrict__ col_src, int ncols,
         ctrl[kDense] = 0;
         ctrl[kDenseReq] = 0;
         ctrl[kDepth] = 0;
+        ctrl[kFrozenAcc] = 0;
+        ctrl[kDone] = 0;
     }
 }
 
@@ -550,21 +554,59 @@ __global__ void aesc_pull_combine(const uint32_t* __restrict__ heavy_rows,
     flush_degsum(bds, ds0, ds1, lane, degsum_next);
 }
 
-// Hook (aesc.hpp:581-588) at depth l+1 for the columns that just stepped.
-__global__ void aesc_hook(const uint32_t* __restrict__ col_src,
-                          const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
-                          const uint32_t* __restrict__ tau_slot, const double* __restrict__ Pn,
-                          const unsigned long long* __restrict__ ctrl, double* __restrict__ g_hat) {
+
+// K3f + K3b of the next depth in one launch (block per column): the hook of
+// depth l+1 for the columns that stepped, then the crossover check of depth
+// l+1 (aesc_check's per-column test); the last block to finish publishes the
+// new active / frozen masks and advances the depth. Every block reads the
+// control block before the last one rewrites it, so the hook and the checks
+// see the masks of depth l exactly as the separate kernels did.
+__global__ void __launch_bounds__(128)
+    aesc_hook_check(const uint32_t* __restrict__ col_src, const uint32_t* __restrict__ col_tau,
+                    const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
+                    const uint32_t* __restrict__ tau_slot, const double* __restrict__ Pn, AescParams p,
+                    const unsigned long long* __restrict__ degsum_cur, unsigned long long* __restrict__ degsum_next,
+                    uint32_t* __restrict__ tt, uint32_t* __restrict__ ucount_next, unsigned long long* ctrl,
+                    double* __restrict__ g_hat) {
+    __shared__ bool last;
     const int c = blockIdx.x;
-    if (!((ctrl[kActive] >> c) & 1ull)) return;
-    const uint32_t depth = uint32_t(ctrl[kDepth]);  // l + 1 (advanced by aesc_check)
-    const uint32_t src = col_src[c];
-    const uint2 r = csr[src];
-    const double pi = Pn[size_t(src) * kCols + c] * (1.0 / double(r.y));
-    for (uint32_t s = r.x + threadIdx.x; s < r.x + r.y; s += blockDim.x) {
-        if (depth > tau_slot[s]) continue;
-        const uint32_t j = adj[s];
-        g_hat[s] += pi - Pn[size_t(j) * kCols + c] * (1.0 / double(csr[j].y));
+    const unsigned long long active = ctrl[kActive];
+    const uint32_t depth = uint32_t(ctrl[kDepth]);  // l + 1
+    if ((active >> c) & 1ull) {  // hook (aesc.hpp:581-588)
+        const uint32_t src = col_src[c];
+        const uint2 r = csr[src];
+        const double pi = Pn[size_t(src) * kCols + c] * (1.0 / double(r.y));
+        for (uint32_t s = r.x + threadIdx.x; s < r.x + r.y; s += blockDim.x) {
+            if (depth > tau_slot[s]) continue;
+            const uint32_t j = adj[s];
+            g_hat[s] += pi - Pn[size_t(j) * kCols + c] * (1.0 / double(csr[j].y));
+        }
+    }
+    if (threadIdx.x == 0) {  // check of depth l + 1 (aesc.hpp:391-394)
+        degsum_next[c] = 0;
+        if ((active >> c) & 1ull) {
+            const uint32_t src = col_src[c];
+            bool stop = depth >= col_tau[c] || (p.cap >= 0 && int64_t(depth) >= p.cap);
+            if (!stop) stop = budget_reached(p, csr, tau_slot, src, depth, degsum_cur[c]);
+            if (stop) {
+                tt[c] = depth;
+                atomicOr(ctrl + kFrozenAcc, 1ull << c);
+            }
+        }
+        __threadfence();
+        last = atomicAdd(ctrl + kDone, 1ull) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long frozen = atomicExch(ctrl + kFrozenAcc, 0ull);
+        ctrl[kFrozenNow] = frozen;
+        ctrl[kActive] = active & ~frozen;
+        if (ctrl[kDenseReq]) ctrl[kDense] = 1;  // mode switches only between depths
+        ctrl[kDepth] = depth + 1;
+        ctrl[kRowNext] = 0;
+        *ucount_next = 0;
+        ctrl[kDone] = 0;
     }
 }
 
@@ -1109,10 +1151,12 @@ struct Engine {
         const int grid_pull = occ_grid(aesc_pull), grid_comb = occ_grid(aesc_pull_combine);
         // One depth (aesc.hpp:391-397 + hook): every argument except the
         // buffer parity is fixed, the depth itself lives on the device.
+        // The check of depth 0 runs once here; every depth ends with the hook
+        // and the check of the next depth fused (aesc_hook_check).
+        aesc_check<<<1, kCols, 0, s>>>(UC + 1, st->col_src.as<uint32_t>(), st->col_tau.as<uint32_t>(), csr, tsl,
+                                       p, DS[0], DS[1], ttd, ctrl);
+        ++launches;
         auto enqueue_depth = [&](int cur) {
-            aesc_check<<<1, kCols, 0, s>>>(UC + (cur ^ 1), st->col_src.as<uint32_t>(),
-                                           st->col_tau.as<uint32_t>(), csr, tsl, p, DS[cur], DS[cur ^ 1],
-                                           ttd, ctrl);
             aesc_rho_expand<<<grid, 256, 0, s>>>(P[cur], csr, adj, M[cur], UL[cur], UC + cur, UL[cur ^ 1],
                                                  UC + (cur ^ 1), flag, tflag, tlist, tcount, ctrl, n,
                                                  st->R.as<double>(), st->bits.as<uint32_t>(), words());
@@ -1133,10 +1177,11 @@ struct Engine {
                     st->heavy_rows.as<uint32_t>(), st->piece_off.as<uint32_t>(), st->nheavy, csr,
                     st->part.as<double>(), st->part_mask.as<unsigned long long>(), P[cur ^ 1],
                     Q[cur ^ 1], M[cur ^ 1], flag, DS[cur ^ 1], ctrl);
-            aesc_hook<<<kCols, 128, 0, s>>>(st->col_src.as<uint32_t>(), csr, adj, tsl, P[cur ^ 1], ctrl,
-                                            g_hat_dev);
+            aesc_hook_check<<<kCols, 128, 0, s>>>(st->col_src.as<uint32_t>(), st->col_tau.as<uint32_t>(), csr, adj,
+                                                  tsl, P[cur ^ 1], p, DS[cur ^ 1], DS[cur], ttd, UC + cur, ctrl,
+                                                  g_hat_dev);
         };
-        const uint32_t per_depth = st->npieces ? 6 : 4;
+        const uint32_t per_depth = st->npieces ? 5 : 3;
         if (!depth_graph) {
             // depths_per_graph() depths (even, so the buffer parity returns to 0)
             // captured once per estimator call and replayed for every batch
@@ -1154,6 +1199,13 @@ struct Engine {
             launches += per_depth * depths_per_graph();
             if (read_ctrl(kActive) == 0) break;
         }
+        // Columns frozen by the check fused into a replay's last depth get
+        // their rho from the next depth's first kernel, which no replay runs:
+        // run it here (a replay has an even number of depths, so that depth
+        // has parity 0; the expansion half exits, nothing is active).
+        aesc_rho_expand<<<grid, 256, 0, s>>>(P[0], csr, adj, M[0], UL[0], UC, UL[1], UC + 1, flag, tflag, tlist,
+                                             tcount, ctrl, n, st->R.as<double>(), st->bits.as<uint32_t>(), words());
+        ++launches;
         SABA_CUDA_CHECK(cudaGetLastError());
         if (parity) *parity = 0;
         last_dense = read_ctrl(kDense) != 0;
