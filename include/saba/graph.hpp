@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <istream>
 #include <memory>
+#include <mutex>
 #include <ostream>
 #include <span>
 #include <string>
@@ -168,7 +169,12 @@ public:
     }
 
     /// The device replica on `device` (created on first use; shared by copies).
+    /// Thread-safe: the reference's Graph may be read from any number of
+    /// threads at once (graph.hpp:24-27), so the lazy creation is locked, and
+    /// libsaba_cuda serialises calls on one handle (saba_cu_graph::mu).
     saba_cu_graph* device_handle(int device = 0) const {
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lock(mu);
         if (!dev_ || dev_->device != device) {
             saba_cu_graph* h = nullptr;
             detail::raise_on(saba_cu_graph_create(offsets_.data(), adjacency_.data(), n_,

@@ -112,6 +112,20 @@ typedef struct saba_cu_graph saba_cu_graph;
 
 SABA_API int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uint32_t n,
                          uint64_t two_m, int device, saba_cu_graph** out);
+/* Multi-device handle: one replica of the CSR on each of
+ * devices[0..ndev) — repeats allowed (logical shards sharing one GPU, each
+ * with its own replica and workspaces). The handle is the replica on
+ * devices[0]. saba_cu_walk_campaign and saba_cu_aesc given such a handle run
+ * one shard per replica, one host thread each, and combine once on
+ * devices[0] (an NCCL reduce over NVLink when the devices are distinct and
+ * libnccl.so.2 can be opened; peer copies + an add kernel otherwise). The
+ * results are bit-identical to a one-device run: counts are integer sums and
+ * every g_hat slot has a single writer. The C++ drop-in maps
+ * CampaignConfig/AescConfig::threads to the device count (walker.hpp:372,
+ * aesc.hpp:47: 0 = all). */
+SABA_API int saba_cu_graph_create_multi(const uint32_t* offsets, const uint32_t* adjacency, uint32_t n,
+                                        uint64_t two_m, const int* devices, int ndev, saba_cu_graph** out);
+SABA_API int saba_cu_graph_replica_count(const saba_cu_graph* g);
 SABA_API int saba_cu_graph_destroy(saba_cu_graph* g);
 SABA_API uint32_t saba_cu_graph_vertex_count(const saba_cu_graph* g);
 SABA_API uint64_t saba_cu_graph_edge_count(const saba_cu_graph* g);
@@ -228,6 +242,7 @@ typedef struct {
     int32_t clamped;
     uint32_t max_tau;
     uint32_t launches;
+    uint32_t replicas;         /* device replicas that ran shards of this call */
 } saba_cu_aesc_report;
 
 /* walk_budget (aesc.hpp:117-126). */
@@ -239,14 +254,39 @@ SABA_API int saba_cu_truncated_lengths(saba_cu_graph* g, double epsilon, uint32_
                               double* lambda_hat, int* clamped);
 
 /* aesc (aesc.hpp:636-708). sources == NULL: every vertex (the full
- * estimator); otherwise only the listed sources (their g_hat slots and
- * tau_tilde entries; others left 0, s_hat not formed). Outputs (host):
- * g_hat[2m] per directed slot, s_hat[m] per edge id (may be NULL), tau[m],
- * tau_tilde[n]. Sharding: source list cut as s ≡ shard_index (mod shard_count). */
+ * estimator); otherwise only the listed sources (deduplicated: a repeated
+ * source is idempotent, as in the reference's per-source loop; their g_hat
+ * slots and tau_tilde entries; others left 0, s_hat not formed). Outputs
+ * (host): g_hat[2m] per directed slot, s_hat[m] per edge id (may be NULL),
+ * tau[m], tau_tilde[n]. Sharding: shard shard_index of shard_count runs the
+ * sources saba_cu_aesc_shard_sources returns; every source runs on exactly one
+ * shard, so summing the shards' g_hat is exact (single writer per slot). */
 SABA_API int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_t* sources,
                  uint64_t source_count, uint32_t shard_index, uint32_t shard_count,
                  double* g_hat_out, double* s_hat_out, uint32_t* tau_out,
                  uint32_t* tau_tilde_out, saba_cu_aesc_report* report);
+
+/* aesc with the estimate left on the device, for callers that combine
+ * shards themselves (one process per GPU: an NCCL all-reduce of g_hat_dev is
+ * exact, each slot having one writer) and then form s_hat with
+ * saba_cu_symmetrise. g_hat_dev: 2m doubles on g's device, fully written
+ * (0 outside this shard's sources' slots), ordered on `stream`; tau_out[m]
+ * and tau_tilde_out[n] are host outputs and may be NULL. */
+SABA_API int saba_cu_aesc_device(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_t* sources,
+                                 uint64_t source_count, uint32_t shard_index, uint32_t shard_count,
+                                 double* g_hat_dev, uint32_t* tau_out, uint32_t* tau_tilde_out, void* stream,
+                                 saba_cu_aesc_report* report);
+/* K5 (aesc.hpp:702-706) on device buffers: s_hat_dev[e] = g_hat_dev[u->v] +
+ * g_hat_dev[v->u] for every edge id e = {u, v}; enqueued on `stream`. */
+SABA_API int saba_cu_symmetrise(saba_cu_graph* g, const double* g_hat_dev, double* s_hat_dev, void* stream);
+
+/* The distinct sources shard shard_index of shard_count runs (sources ==
+ * NULL: all vertices; host-only, needs no device): cost-stratified — ascending degree (the walk work of
+ * a source is ~tau^3/d at a uniform tau, aesc.hpp:103-110), dealt to the
+ * shards in snake order. out may be NULL to query *out_count. */
+SABA_API int saba_aesc_shard_sources(const uint32_t* offsets, uint32_t n, const uint32_t* sources,
+                                     uint64_t source_count, uint32_t shard_index, uint32_t shard_count,
+                                     uint32_t* out, uint64_t* out_count);
 
 /* propagate_landing_probabilities (aesc.hpp:406-422): dense prob_out[n] at
  * the switch depth; *depth_out = tau~. tau[m] per edge id. */

@@ -45,6 +45,11 @@ class _OracleCfg(C.Structure):
                 ("threads", C.c_int)]
 
 
+class _Csr(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("m", C.c_uint64), ("off", C.POINTER(C.c_uint32)),
+                ("adj", C.POINTER(C.c_uint32))]
+
+
 class _RefCfg(C.Structure):
     _fields_ = _OracleCfg._fields_ + [("mode", C.c_int), ("lanes", C.c_uint32)]
 
@@ -105,9 +110,36 @@ class Oracle:
                                          C.c_uint64, u64p]
         L.oracle_propagate.argtypes = [u32p, u32p, C.c_uint32, C.c_uint64, C.c_uint32, u32p, u32p,
                                        C.c_double, C.c_double, C.c_int64, f64p, u32p]
+        L.oracle_csr_free.argtypes = [C.POINTER(_Csr)]
+        L.oracle_gen_erdos_renyi.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(_Csr)]
+        L.oracle_gen_rmat.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double,
+                                      C.c_uint64, C.c_int, C.POINTER(_Csr)]
+        L.oracle_gen_chung_lu.argtypes = [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                          C.c_int, C.POINTER(_Csr)]
         L.oracle_aesc.restype = C.c_int
         L.oracle_aesc.argtypes = [u32p, u32p, C.c_uint32, C.c_uint64, C.POINTER(_OracleCfg),
                                   u32p, C.c_uint64, f64p, f64p, u32p, u32p, f64p, u64p, u64p]
+
+    # -- BASELINE graphs (oracle_gen.c): (offsets, adjacency) numpy arrays
+    def _csr(self, fn, *args):
+        c = _Csr()
+        _raise(fn(*args, C.byref(c)), fn.__name__)
+        try:
+            off = np.ctypeslib.as_array(c.off, shape=(c.n + 1,)).copy()
+            adj = np.ctypeslib.as_array(c.adj, shape=(max(2 * c.m, 1),))[: 2 * c.m].copy()
+        finally:
+            self.lib.oracle_csr_free(C.byref(c))
+        return off, adj
+
+    def gen_erdos_renyi(self, n, m, seed):
+        return self._csr(self.lib.oracle_gen_erdos_renyi, n, m, seed)
+
+    def gen_rmat(self, scale, edge_factor, a=0.57, b=0.19, c=0.19, seed=1, keep_lcc=True):
+        return self._csr(self.lib.oracle_gen_rmat, scale, edge_factor, a, b, c, seed, int(keep_lcc))
+
+    def gen_chung_lu(self, n, gamma=2.2, mean_degree=78.0, max_degree=30000.0, seed=1, keep_lcc=True):
+        return self._csr(self.lib.oracle_gen_chung_lu, n, gamma, mean_degree, max_degree, seed,
+                         int(keep_lcc))
 
     # -- primitives
     def mix64(self, x): return self.lib.oracle_mix64(x)

@@ -96,6 +96,22 @@ int oracle_aesc(const uint32_t* off, const uint32_t* adj, uint32_t n, uint64_t m
                 double* g_hat, double* s_hat, uint32_t* tau, uint32_t* tau_tilde,
                 double* lambda_hat, uint64_t* pairs, uint64_t* steps);
 
+/* BASELINE generators (oracle_gen.c): CSR identical to the product's
+ * saba_gen_* / saba_cu_gen_*; release with oracle_csr_free. Return 0 ok,
+ * 1 invalid argument. */
+typedef struct {
+    uint32_t n;
+    uint64_t m;
+    uint32_t* off;
+    uint32_t* adj;
+} oracle_csr;
+void oracle_csr_free(oracle_csr* g);
+int oracle_gen_erdos_renyi(uint32_t n, uint64_t m, uint64_t seed, oracle_csr* out);
+int oracle_gen_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                    uint64_t seed, int keep_lcc, oracle_csr* out);
+int oracle_gen_chung_lu(uint32_t n, double gamma, double mean_degree, double max_degree,
+                        uint64_t seed, int keep_lcc, oracle_csr* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,7 +54,7 @@ class AescReportC(C.Structure):
                 ("total_walk_pairs", C.c_uint64), ("total_walk_steps", C.c_uint64),
                 ("edge_visits", C.c_uint64), ("sources", C.c_uint64),
                 ("lambda_hat", C.c_double), ("bipartite", C.c_int32), ("clamped", C.c_int32),
-                ("max_tau", C.c_uint32), ("launches", C.c_uint32)]
+                ("max_tau", C.c_uint32), ("launches", C.c_uint32), ("replicas", C.c_uint32)]
 
 
 vp = C.c_void_p
@@ -86,6 +86,9 @@ SIGNATURES = {
     "saba_hgraph_data": (C.c_int, [vp, C.POINTER(u32p), C.POINTER(u32p)]),
     "saba_hgraph_free": (None, [vp]),
     "saba_cu_graph_create": (C.c_int, [u32p, u32p, C.c_uint32, C.c_uint64, C.c_int, vpp]),
+    "saba_cu_graph_create_multi": (C.c_int, [u32p, u32p, C.c_uint32, C.c_uint64, C.POINTER(C.c_int),
+                                             C.c_int, vpp]),
+    "saba_cu_graph_replica_count": (C.c_int, [vp]),
     "saba_cu_graph_destroy": (C.c_int, [vp]),
     "saba_cu_graph_vertex_count": (C.c_uint32, [vp]),
     "saba_cu_graph_edge_count": (C.c_uint64, [vp]),
@@ -104,6 +107,12 @@ SIGNATURES = {
                                             u32p, f64p, C.POINTER(C.c_int)]),
     "saba_cu_aesc": (C.c_int, [vp, C.POINTER(AescConfigC), u32p, C.c_uint64, C.c_uint32,
                                C.c_uint32, f64p, f64p, u32p, u32p, C.POINTER(AescReportC)]),
+    "saba_cu_aesc_device": (C.c_int, [vp, C.POINTER(AescConfigC), u32p, C.c_uint64, C.c_uint32,
+                                      C.c_uint32, C.c_void_p, u32p, u32p, C.c_void_p,
+                                      C.POINTER(AescReportC)]),
+    "saba_cu_symmetrise": (C.c_int, [vp, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "saba_aesc_shard_sources": (C.c_int, [u32p, C.c_uint32, u32p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                          u32p, u64p]),
     "saba_cu_propagate": (C.c_int, [vp, C.c_uint32, u32p, C.c_double, C.c_double, C.c_int64,
                                     f64p, u32p]),
     "saba_cu_estimate_edge": (C.c_int, [vp, C.c_uint32, C.c_uint32, f64p, C.c_uint32,

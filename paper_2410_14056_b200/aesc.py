@@ -130,8 +130,8 @@ def _is_connected(g: Graph) -> bool:
 def aesc(g: Graph, cfg: AescConfig, *, sources=None, shard_index: int = 0, shard_count: int = 1,
          device: int = 0) -> CentralityEstimate:
     """aesc.hpp:636-708 on one B200. `sources` restricts the estimator to a
-    source subset (SURVEY §8d protocol); sharding takes sources
-    s_i with i % shard_count == shard_index."""
+    source subset (SURVEY §8d protocol), deduplicated; shard `shard_index`
+    of `shard_count` runs the sources aesc_shard_sources() returns."""
     n, m = g.n, g.m
     g_hat = np.zeros(2 * m, np.float64)
     full = sources is None and shard_count == 1
@@ -187,10 +187,19 @@ def write_centrality_tsv(out, g: Graph, values) -> None:
         out.write(f"{int(e[i, 0])}\t{int(e[i, 1])}\t{values[i]:.6g}\n")
 
 
-def aesc_shard_sources(sources, shard_index: int, shard_count: int) -> np.ndarray:
-    """Sources of one shard: every shard_count-th entry starting at
-    shard_index, the interleaved split aesc.cu uses (per-source cost varies
-    ~85x and correlates with vertex id, SURVEY §7 hard part 5)."""
+def aesc_shard_sources(g: Graph, sources, shard_index: int, shard_count: int) -> np.ndarray:
+    """The distinct sources shard `shard_index` of `shard_count` runs
+    (sources=None: every vertex), exactly as saba_cu_aesc cuts them:
+    ascending degree — a source's walk work falls as ~tau^3/d — dealt to the
+    shards in snake order, so every shard gets the same cost profile.
+    Host-only (no device needed)."""
     if not 0 <= shard_index < shard_count:
         raise ValueError("bad shard index/count")
-    return np.ascontiguousarray(np.asarray(sources, np.uint32)[shard_index::shard_count])
+    src = None if sources is None else np.ascontiguousarray(sources, np.uint32)
+    cnt = C.c_uint64()
+    args = (L.ptr(g.offsets, L.u32p), g.n, L.ptr(src, L.u32p), 0 if src is None else len(src),
+            shard_index, shard_count)
+    L.check(L.lib().saba_aesc_shard_sources(*args, None, C.byref(cnt)), "aesc_shard_sources")
+    out = np.zeros(cnt.value, np.uint32)
+    L.check(L.lib().saba_aesc_shard_sources(*args, L.ptr(out, L.u32p), C.byref(cnt)), "aesc_shard_sources")
+    return out

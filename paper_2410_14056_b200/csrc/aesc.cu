@@ -53,6 +53,7 @@
 #include <exception>
 #include <memory>
 #include <thread>
+#include <atomic>
 #include <cmath>
 #include <vector>
 
@@ -92,6 +93,7 @@ struct AescState {
     cudaStream_t stream = nullptr;       // propagation (and everything else)
     cudaStream_t stream_walk = nullptr;  // walk phase of the batch workers
     uint64_t* h_ctrl = nullptr;  // pinned mirror of the control block
+    bool slot_edge_ready = false;  // slot_edge_d holds the slot -> edge map (K5)
     ~AescState() {
         if (stream) cudaStreamDestroy(stream);
         if (stream_walk) cudaStreamDestroy(stream_walk);
@@ -118,7 +120,7 @@ namespace {
 
 // Control block (device): active mask, frozen-at-this-depth mask, dense flag.
 enum { kActive = 0, kFrozenNow = 1, kDense = 2, kDenseReq = 3, kDepth = 4, kRowNext = 5, kFrozenAcc = 6,
-       kDone = 7, kCtrlWords = 8 };
+       kDone = 7, kEdgeVisits = 8, kCtrlWords = 9 };
 
 struct AescParams {
     double eps, delta, log_term;  // log_term = log(4m/delta) (aesc.hpp:109)
@@ -211,7 +213,7 @@ __global__ void aesc_check(uint32_t* __restrict__ ucount_next, const uint32_t* _
                            const uint32_t* __restrict__ tau_slot, AescParams p,
                            const unsigned long long* __restrict__ degsum_cur,
                            unsigned long long* __restrict__ degsum_next, uint32_t* __restrict__ tt,
-                           unsigned long long* __restrict__ ctrl) {
+                           unsigned long long* __restrict__ ctrl, unsigned long long* __restrict__ edge_visits) {
     __shared__ unsigned long long frozen;
     const int c = threadIdx.x;
     const uint32_t l = uint32_t(ctrl[kDepth]);
@@ -226,6 +228,8 @@ __global__ void aesc_check(uint32_t* __restrict__ ucount_next, const uint32_t* _
         if (stop) {
             tt[c] = l;
             atomicOr(&frozen, 1ull << c);
+        } else {  // edge-visits of the push l -> l+1 (aesc.hpp:306-326)
+            atomicAdd(edge_visits, degsum_cur[c]);
         }
     }
     __syncthreads();
@@ -558,20 +562,28 @@ __global__ void aesc_pull_combine(const uint32_t* __restrict__ heavy_rows,
 // K3f + K3b of the next depth in one launch (block per column): the hook of
 // depth l+1 for the columns that stepped, then the crossover check of depth
 // l+1 (aesc_check's per-column test); the last block to finish publishes the
-// new active / frozen masks and advances the depth. Every block reads the
-// control block before the last one rewrites it, so the hook and the checks
-// see the masks of depth l exactly as the separate kernels did.
+// new active / frozen masks and advances the depth. Thread 0 of each block
+// stages the control words in shared memory and the block passes a barrier
+// before that thread counts the block as done, so no thread of any block can
+// read ctrl after the last block rewrites it: the hook and the checks see the
+// masks of depth l exactly as the separate kernels did, by construction.
 __global__ void __launch_bounds__(128)
     aesc_hook_check(const uint32_t* __restrict__ col_src, const uint32_t* __restrict__ col_tau,
                     const uint2* __restrict__ csr, const uint32_t* __restrict__ adj,
                     const uint32_t* __restrict__ tau_slot, const double* __restrict__ Pn, AescParams p,
                     const unsigned long long* __restrict__ degsum_cur, unsigned long long* __restrict__ degsum_next,
                     uint32_t* __restrict__ tt, uint32_t* __restrict__ ucount_next, unsigned long long* ctrl,
-                    double* __restrict__ g_hat) {
+                    double* __restrict__ g_hat, unsigned long long* __restrict__ edge_visits) {
     __shared__ bool last;
+    __shared__ unsigned long long s_active, s_depth;
     const int c = blockIdx.x;
-    const unsigned long long active = ctrl[kActive];
-    const uint32_t depth = uint32_t(ctrl[kDepth]);  // l + 1
+    if (threadIdx.x == 0) {
+        s_active = ctrl[kActive];
+        s_depth = ctrl[kDepth];
+    }
+    __syncthreads();
+    const unsigned long long active = s_active;
+    const uint32_t depth = uint32_t(s_depth);  // l + 1
     if ((active >> c) & 1ull) {  // hook (aesc.hpp:581-588)
         const uint32_t src = col_src[c];
         const uint2 r = csr[src];
@@ -591,6 +603,8 @@ __global__ void __launch_bounds__(128)
             if (stop) {
                 tt[c] = depth;
                 atomicOr(ctrl + kFrozenAcc, 1ull << c);
+            } else {  // the push of depth l+1 -> l+2 visits every support slot
+                atomicAdd(edge_visits, degsum_cur[c]);
             }
         }
         __threadfence();
@@ -1046,7 +1060,8 @@ struct Engine {
         buf<uint64_t>(st->degsum[0], kCols);
         buf<uint64_t>(st->degsum[1], kCols);
         buf<uint32_t>(st->tt, kCols);
-        buf<uint64_t>(st->ctrl, kCtrlWords);
+        // kEdgeVisits accumulates over the batches of one estimator call
+        SABA_CUDA_CHECK(cudaMemsetAsync(buf<uint64_t>(st->ctrl, kCtrlWords), 0, sizeof(uint64_t) * kCtrlWords, s));
     }
 
     // Rows with degree > kHeavy and their fixed pieces of kHeavy neighbours.
@@ -1154,7 +1169,7 @@ struct Engine {
         // The check of depth 0 runs once here; every depth ends with the hook
         // and the check of the next depth fused (aesc_hook_check).
         aesc_check<<<1, kCols, 0, s>>>(UC + 1, st->col_src.as<uint32_t>(), st->col_tau.as<uint32_t>(), csr, tsl,
-                                       p, DS[0], DS[1], ttd, ctrl);
+                                       p, DS[0], DS[1], ttd, ctrl, ctrl + kEdgeVisits);
         ++launches;
         auto enqueue_depth = [&](int cur) {
             aesc_rho_expand<<<grid, 256, 0, s>>>(P[cur], csr, adj, M[cur], UL[cur], UC + cur, UL[cur ^ 1],
@@ -1179,7 +1194,7 @@ struct Engine {
                     Q[cur ^ 1], M[cur ^ 1], flag, DS[cur ^ 1], ctrl);
             aesc_hook_check<<<kCols, 128, 0, s>>>(st->col_src.as<uint32_t>(), st->col_tau.as<uint32_t>(), csr, adj,
                                                   tsl, P[cur ^ 1], p, DS[cur ^ 1], DS[cur], ttd, UC + cur, ctrl,
-                                                  g_hat_dev);
+                                                  g_hat_dev, ctrl + kEdgeVisits);
         };
         const uint32_t per_depth = st->npieces ? 5 : 3;
         if (!depth_graph) {
@@ -1536,6 +1551,46 @@ struct DeviceSpmv {
     }
 };
 
+}  // namespace
+
+// The distinct sources of one shard. A repeated source is idempotent in the
+// reference's per-source loop (each aesc_source call rewrites its own g_hat
+// slots, aesc.hpp:572-577), but one batch column per occurrence would add its
+// estimate twice, so the list is deduplicated first. Shards are cut
+// cost-stratified: with a uniform tau the walk work of source v is
+// sum_slots n_req * tau ~ tau^3 / d(v) (aesc.hpp:103-110, 478-496) and falls
+// with degree, while tau~ grows as the degree falls (the ~85x spread of
+// SURVEY §7); sources in ascending-degree order (ties by id) are dealt to the
+// shards in snake order 0..N-1, N-1..0, so every shard gets the same degree
+// profile. Each source runs on exactly one shard, so the sum over shards is
+// exact and results are identical for any shard count.
+std::vector<uint32_t> shard_sources(const uint32_t* off, uint32_t n, const uint32_t* sources, uint64_t count,
+                                    uint32_t shard_index, uint32_t shard_count) {
+    std::vector<uint32_t> all;
+    if (sources) {
+        all.assign(sources, sources + count);
+        for (uint32_t v : all) check_arg(v < n, "source out of range");
+        std::sort(all.begin(), all.end());
+        all.erase(std::unique(all.begin(), all.end()), all.end());
+    } else {
+        all.resize(n);
+        for (uint32_t v = 0; v < n; ++v) all[v] = v;
+    }
+    if (shard_count <= 1) return all;
+    auto deg = [&](uint32_t v) { return off[v + 1] - off[v]; };
+    std::stable_sort(all.begin(), all.end(), [&](uint32_t a, uint32_t b) { return deg(a) < deg(b); });
+    std::vector<uint32_t> mine;
+    mine.reserve(all.size() / shard_count + 1);
+    for (uint64_t i = 0; i < all.size(); ++i) {
+        const uint64_t r = i % (2ull * shard_count);
+        const uint64_t shard = r < shard_count ? r : 2ull * shard_count - 1 - r;
+        if (shard == shard_index) mine.push_back(all[i]);
+    }
+    return mine;
+}
+
+namespace {
+
 AescParams make_params(const saba_cu_graph* g, double eps, double delta, int64_t cap) {
     AescParams p{};
     p.eps = eps;
@@ -1545,6 +1600,260 @@ AescParams make_params(const saba_cu_graph* g, double eps, double delta, int64_t
     p.n = g->n;
     p.m = g->m;
     return p;
+}
+
+// K5 on `st`: s_hat[e] = g_hat[u->v] + g_hat[v->u] (aesc.hpp:702-706). The
+// slot -> edge map is uploaded once per handle.
+void enqueue_symmetrise(saba_cu_graph* g, const double* d_g, double* d_s, cudaStream_t st) {
+    if (!g->aesc) g->aesc = new AescState[kWorkspaces];
+    AescState& a = g->aesc[0];
+    if (!a.slot_edge_ready) {
+        const IdVec& se = slot_edges(g);
+        uint32_t* d_se = static_cast<uint32_t*>(a.slot_edge_d.ensure(sizeof(uint32_t) * 2 * g->m, st));
+        copy_h2d(d_se, se.data(), sizeof(uint32_t) * 2 * g->m, st);
+        a.slot_edge_ready = true;
+    }
+    aesc_symmetrise<<<g->sm_count * 4, 256, 0, st>>>(g->d_csr, g->d_adj, a.slot_edge_d.as<uint32_t>(), g->n,
+                                                     d_g, d_s);
+    SABA_CUDA_CHECK(cudaGetLastError());
+}
+
+// One estimator call: the plan (once, on the first replica), then this
+// shard's sources in batches of 64 over every replica of the handle (one
+// multi-device handle = one shard per replica) and every batch worker of a
+// replica, handed out dynamically (a shared batch counter: per-source cost
+// varies ~85x), and finally one combine of the replicas' g_hat on
+// the first replica. A column's arithmetic never depends on its batch, its
+// worker or its replica, so the result is identical for any device count.
+struct AescRun {
+    Plan plan;
+    std::vector<saba_cu_graph*> reps;
+    std::vector<double*> d_g;       // per replica: its g_hat (2m), combined into d_g[0]
+    std::vector<uint32_t> tt_all;   // tau~ per vertex (0 outside this call's sources)
+    uint64_t pairs = 0, steps = 0, edge_visits = 0, nsources = 0;
+    float prop_ms = 0.f, walk_ms = 0.f;
+    uint32_t launches = 0;
+    double seconds = 0.0, plan_seconds = 0.0;
+    cudaStream_t root_stream = nullptr;
+    const char* combine = "none";
+};
+
+void fill_aesc_report(const AescRun& run, saba_cu_aesc_report* rep) {
+    saba_cu_aesc_report r{};
+    r.seconds = run.seconds;
+    r.plan_seconds = run.plan_seconds;
+    r.propagation_ms = run.prop_ms;
+    r.walk_ms = run.walk_ms;
+    r.total_walk_pairs = run.pairs;
+    r.total_walk_steps = run.steps;
+    r.edge_visits = run.edge_visits;
+    r.sources = run.nsources;
+    r.lambda_hat = run.plan.lambda_hat;
+    r.bipartite = run.plan.bipartite;
+    r.clamped = run.plan.clamped;
+    r.max_tau = run.plan.max_tau;
+    r.launches = run.launches;
+    r.replicas = uint32_t(run.reps.size());
+    *rep = r;
+}
+
+void aesc_run(saba_cu_graph* g, const saba_cu_aesc_config& cfg, const uint32_t* sources, uint64_t source_count,
+              uint32_t shard_index, uint32_t shard_count, bool need_slot_edges, AescRun& out) {
+    const bool trace = getenv("SABA_TRACE") != nullptr;
+    auto T = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!trace) return;
+        const auto T1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[saba] aesc %-26s %9.2f ms\n", what, std::chrono::duration<double, std::milli>(T1 - T).count());
+        T = T1;
+    };
+    const auto t_plan0 = std::chrono::steady_clock::now();
+    const auto& hadj = host_adj(g);
+    lap("host adjacency");
+    const HostCsr h{g->n, g->m, g->h_off.data(), hadj.data()};
+    check_data(host_is_connected(h), "aesc: spanning centrality requires a connected graph");
+    lap("connectivity");
+    // slot -> edge ids: only per-edge plans and the s_hat symmetrisation need them
+    const uint32_t* se = cfg.per_edge_tau || need_slot_edges ? slot_edges(g).data() : nullptr;
+    lap("slot edges");
+    // aesc.hpp:649: the plan is built for epsilon / 2
+    DeviceSpmv dev{g};
+    const SpmvFn spmv = dev.fn();
+    out.plan = host_truncated_lengths(h, se, cfg.epsilon / 2.0, cfg.power_iterations, cfg.max_truncation,
+                                      cfg.per_edge_tau != 0, &spmv);
+    const Plan& plan = out.plan;
+    const auto t_plan1 = std::chrono::steady_clock::now();
+    out.plan_seconds = std::chrono::duration<double>(t_plan1 - t_plan0).count();
+    lap("truncation plan");
+    const uint32_t n = g->n;
+    const uint64_t m = g->m;
+    std::vector<uint32_t> list = shard_sources(g->h_off.data(), n, sources, source_count, shard_index, shard_count);
+    out.nsources = list.size();
+    // batches by descending degree (tau~ correlates with degree; batching
+    // never changes a column's arithmetic)
+    std::stable_sort(list.begin(), list.end(), [&](uint32_t a, uint32_t b) {
+        return g->h_off[a + 1] - g->h_off[a] > g->h_off[b + 1] - g->h_off[b];
+    });
+    // tau per directed slot: a constant for a uniform plan (the default)
+    std::vector<uint32_t> ts_v;
+    SlotTau ts{nullptr, plan.tau.empty() ? 0u : plan.tau[0]};
+    if (!plan.uniform) {
+        ts_v.resize(2 * m);
+#pragma omp parallel for schedule(static)
+        for (int64_t sl = 0; sl < int64_t(2 * m); ++sl) ts_v[sl] = plan.tau[se[sl]];
+        ts.v = ts_v.data();
+    }
+    lap("tau per slot");
+    out.reps = replicas_of(g);
+    const uint32_t R = uint32_t(out.reps.size());
+    static const int workers_env = [] {  // SABA_AESC_WORKERS=1|2 overrides
+        const char* e = getenv("SABA_AESC_WORKERS");
+        return e ? std::max(1, std::min(kWorkspaces, atoi(e))) : 0;
+    }();
+    const size_t nbatches = (list.size() + kCols - 1) / kCols;
+    // (measured: 3 workers gain nothing on cfg3/cfg4; 2 beat 1 on cfg3 and,
+    // since the walk phase got cheaper, on the shallow cfg5 plan too: -11%)
+    const int nworkers = workers_env ? workers_env : (nbatches > R ? kWorkspaces : 1);
+    std::vector<std::unique_ptr<Engine>> engines;  // replica-major: engines[r * nworkers + w]
+    std::vector<std::unique_lock<std::recursive_mutex>> locks;
+    out.d_g.assign(R, nullptr);
+    for (uint32_t r = 0; r < R; ++r) {
+        saba_cu_graph* rg = out.reps[r];
+        if (r) locks.emplace_back(rg->mu);  // replica 0 is g (held by the caller)
+        DeviceScope scope(rg->device);
+        if (fat_fits_l2(rg) && aesc_fat_enabled())
+            ensure_fat(rg);  // before the workers start
+        else if (plan.max_tau < kShortWalk && aesc_fat16_enabled())
+            ensure_fat16(rg);
+        for (int w = 0; w < nworkers; ++w) {
+            engines.emplace_back(new Engine(rg, w));
+            Engine& E = *engines.back();
+            E.p = make_params(rg, cfg.epsilon, cfg.delta, cfg.switch_depth_cap);
+            E.p.bip_init = plan.bipartite ? 1.0 / (2.0 * double(m)) : 0.0;  // aesc.hpp:657
+            E.p.uniform_tau = plan.uniform ? 1 : 0;
+            E.p.tau_uniform = plan.tau.empty() ? 0 : plan.tau[0];
+            E.upload_tau(ts);
+        }
+        Engine& E0 = *engines[size_t(r) * nworkers];
+        double* d_g = static_cast<double*>(E0.st->g_hat.ensure(sizeof(double) * 2 * m, E0.s));
+        SABA_CUDA_CHECK(cudaMemsetAsync(d_g, 0, sizeof(double) * 2 * m, E0.s));
+        out.d_g[r] = d_g;
+        for (int w = 0; w < nworkers; ++w) SABA_CUDA_CHECK(cudaStreamSynchronize(engines[size_t(r) * nworkers + w]->s));
+    }
+    out.root_stream = engines[0]->s;
+    lap("workers ready");
+    out.tt_all.assign(n, 0);
+    const size_t nthreads = engines.size();
+    std::vector<float> prop_ms(nthreads, 0.f), walk_ms(nthreads, 0.f);
+    std::vector<std::exception_ptr> failure(nthreads);
+    std::atomic<size_t> next_batch{0};
+    const auto t0 = std::chrono::steady_clock::now();
+    auto worker = [&](size_t wi) {
+        try {
+            Engine& W = *engines[wi];
+            saba_cu_graph* rg = W.g;
+            double* d_g = out.d_g[wi / nworkers];
+            SABA_CUDA_CHECK(cudaSetDevice(rg->device));
+            cudaEvent_t e0, e1, e2;
+            SABA_CUDA_CHECK(cudaEventCreate(&e0));
+            SABA_CUDA_CHECK(cudaEventCreate(&e1));
+            SABA_CUDA_CHECK(cudaEventCreate(&e2));
+            TileBuilder tb;
+            for (size_t bi = next_batch++; bi < nbatches; bi = next_batch++) {
+                const size_t b0 = bi * kCols;
+                const std::vector<uint32_t> cols(list.begin() + b0, list.begin() + std::min(list.size(), b0 + kCols));
+                const auto h0 = std::chrono::steady_clock::now();
+                SABA_CUDA_CHECK(cudaEventRecord(e0, W.s));
+                const std::vector<uint32_t> tt = W.propagate(cols, d_g);
+                SABA_CUDA_CHECK(cudaEventRecord(e1, W.s));
+                const auto h1 = std::chrono::steady_clock::now();
+                tb.clear();
+                for (size_t c = 0; c < cols.size(); ++c) {
+                    const uint32_t src = cols[c];
+                    out.tt_all[src] = tt[c];  // distinct sources: one writer per entry
+                    const uint32_t lo = g->h_off[src], hi = g->h_off[src + 1], deg_i = hi - lo;
+                    bool any = false;  // aesc.hpp:592-594
+                    for (uint32_t sl = lo; sl < hi && !any; ++sl) any = ts[sl] > tt[c];
+                    if (!any) continue;
+                    const uint64_t src_seed = substream(substream(cfg.master_seed, kAescTag), src);
+                    for (uint32_t sl = lo; sl < hi; ++sl) {
+                        const int64_t tau_eff = int64_t(ts[sl]) - int64_t(tt[c]);
+                        if (tau_eff <= 0) continue;
+                        const uint64_t n_req = walk_budget(uint32_t(tau_eff), cfg.epsilon, cfg.delta, deg_i, m);
+                        check_arg(cfg.switch_depth_cap < 0 || n_req * uint64_t(tau_eff) <= (uint64_t(1) << 26),
+                                  "aesc: walk budget infeasible (switch_depth_cap too aggressive for epsilon)");
+                        tb.add(sl, src, hadj[sl], uint32_t(tau_eff + 1), n_req, substream(src_seed, sl), uint32_t(c));
+                        W.pairs += n_req;
+                        W.steps += 2 * n_req * uint64_t(tau_eff);
+                    }
+                }
+                // sparse supports: skip rho gathers of exact zeros via the bitmap
+                static const int bitmap_mode = [] {  // 0 off, 1 on, 2 auto
+                    const char* e = getenv("SABA_AESC_BITMAP");
+                    return e ? atoi(e) : 2;
+                }();
+                // auto: supports of a few propagation steps are small even
+                // when the batch's union frontier went dense
+                const uint32_t tt_max = *std::max_element(tt.begin(), tt.end());
+                const bool use_bits = bitmap_mode == 1 || (bitmap_mode == 2 && tt_max <= 4);
+                const auto h2 = std::chrono::steady_clock::now();
+                // the propagation above ended with a host sync, and run_tiles
+                // returns after its own, so the two streams never overlap
+                // within one worker
+                run_tiles(rg, W.st, W.st->stream_walk, tb, W.st->R.as<double>(),
+                          use_bits ? W.st->bits.as<uint32_t>() : nullptr, cfg.hash_multiplier, d_g, &W.launches);
+                SABA_CUDA_CHECK(cudaEventRecord(e2, W.s));
+                const auto h3 = std::chrono::steady_clock::now();
+                W.clear_batch(int(cols.size()));
+                SABA_CUDA_CHECK(cudaEventSynchronize(e2));
+                float ta = 0.f, tw = 0.f;
+                SABA_CUDA_CHECK(cudaEventElapsedTime(&ta, e0, e1));
+                SABA_CUDA_CHECK(cudaEventElapsedTime(&tw, e1, e2));
+                prop_ms[wi] += ta;
+                walk_ms[wi] += tw;
+                if (trace) {
+                    const auto h4 = std::chrono::steady_clock::now();
+                    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+                    fprintf(stderr, "[saba] aesc r%d w%zu batch %zu: propagate %.2f ms (device %.2f), tiles %.2f, "
+                            "run_tiles %.2f (device walk %.2f), clear+sync %.2f\n", rg->device, wi, bi, ms(h0, h1), ta,
+                            ms(h1, h2), ms(h2, h3), tw, ms(h3, h4));
+                }
+            }
+            SABA_CUDA_CHECK(cudaStreamSynchronize(W.s));
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            cudaEventDestroy(e2);
+        } catch (...) {
+            failure[wi] = std::current_exception();
+            next_batch = nbatches;  // stop the other workers early
+        }
+    };
+    std::vector<std::thread> threads;
+    for (size_t w = 1; w < nthreads; ++w) threads.emplace_back(worker, w);
+    worker(0);
+    for (auto& t : threads) t.join();
+    SABA_CUDA_CHECK(cudaSetDevice(g->device));
+    for (auto& f : failure)
+        if (f) std::rethrow_exception(f);
+    lap("batches");
+    for (size_t w = 0; w < nthreads; ++w) {
+        Engine& E = *engines[w];
+        DeviceScope scope(E.g->device);
+        out.pairs += E.pairs;
+        out.steps += E.steps;
+        out.launches += E.launches;
+        out.edge_visits += E.read_ctrl(kEdgeVisits);
+        out.prop_ms += prop_ms[w];
+        out.walk_ms += walk_ms[w];
+    }
+    // one combine of the replicas' g_hat (single writer per slot: exact)
+    std::vector<void*> ptrs(out.d_g.begin(), out.d_g.end());
+    std::vector<cudaStream_t> streams;
+    for (uint32_t r = 0; r < R; ++r) streams.push_back(engines[size_t(r) * nworkers]->s);
+    reduce_to_root(out.reps, ptrs, 2 * m, ReduceType::F64, streams);
+    out.combine = last_combine_kind();
+    lap("combine");
+    out.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 }  // namespace
@@ -1559,6 +1868,7 @@ int saba_cu_truncated_lengths(saba_cu_graph* g, double epsilon, uint32_t power_i
                               double* lambda_hat, int* clamped) {
     return guard([&] {
         check_arg(g && tau_out && lambda_hat && clamped, "null argument");
+        std::lock_guard<std::recursive_mutex> lock(g->mu);
         DeviceScope scope(g->device);
         const HostCsr h{g->n, g->m, g->h_off.data(), host_adj(g).data()};
         DeviceSpmv dev{g};
@@ -1579,218 +1889,75 @@ int saba_cu_aesc(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_
         check_arg(g && cfg && g_hat_out && tau_out && tau_tilde_out, "null argument");
         validate_cfg(*cfg);
         check_arg(shard_count >= 1 && shard_index < shard_count, "bad shard index/count");
+        std::lock_guard<std::recursive_mutex> lock(g->mu);
         DeviceScope scope(g->device);
-        const bool trace = getenv("SABA_TRACE") != nullptr;
-        auto T = std::chrono::steady_clock::now();
-        auto lap = [&](const char* what) {
-            if (!trace) return;
-            const auto T1 = std::chrono::steady_clock::now();
-            fprintf(stderr, "[saba] aesc %-26s %9.2f ms\n", what,
-                    std::chrono::duration<double, std::milli>(T1 - T).count());
-            T = T1;
-        };
-        const auto t_plan0 = std::chrono::steady_clock::now();
-        const auto& hadj = host_adj(g);
-        lap("host adjacency");
-        const HostCsr h{g->n, g->m, g->h_off.data(), hadj.data()};
-        check_data(host_is_connected(h), "aesc: spanning centrality requires a connected graph");
-        lap("connectivity");
-        // slot -> edge ids: only per-edge plans and the s_hat symmetrisation need them
         const bool full = sources == nullptr && shard_count == 1;
-        const uint32_t* se = cfg->per_edge_tau || (full && s_hat_out) ? slot_edges(g).data() : nullptr;
-        lap("slot edges");
-        // aesc.hpp:649: the plan is built for epsilon / 2
-        DeviceSpmv dev{g};
-        const SpmvFn spmv = dev.fn();
-        const Plan plan = host_truncated_lengths(h, se, cfg->epsilon / 2.0, cfg->power_iterations,
-                                                 cfg->max_truncation, cfg->per_edge_tau != 0, &spmv);
-        const auto t_plan1 = std::chrono::steady_clock::now();
-        lap("truncation plan");
-        const uint32_t n = g->n;
+        AescRun run;
+        aesc_run(g, *cfg, sources, source_count, shard_index, shard_count, full && s_hat_out, run);
+        saba_cu_graph* root = run.reps[0];
+        cudaStream_t s = run.root_stream;
         const uint64_t m = g->m;
-        for (uint64_t i = 0; i < source_count; ++i) check_arg(sources[i] < n, "source out of range");
-        if (fat_fits_l2(g) && aesc_fat_enabled())
-            ensure_fat(g);  // before the workers start
-        else if (plan.max_tau < kShortWalk && aesc_fat16_enabled())
-            ensure_fat16(g);
-        lap("fat adjacency");
-        Engine E(g);
-        lap("engine");
-        E.p = make_params(g, cfg->epsilon, cfg->delta, cfg->switch_depth_cap);
-        E.p.bip_init = plan.bipartite ? 1.0 / (2.0 * double(m)) : 0.0;  // aesc.hpp:657
-        E.p.uniform_tau = plan.uniform ? 1 : 0;
-        E.p.tau_uniform = plan.tau.empty() ? 0 : plan.tau[0];
-        // tau per directed slot: a constant for a uniform plan (the default)
-        std::vector<uint32_t> ts_v;
-        SlotTau ts{nullptr, plan.tau.empty() ? 0u : plan.tau[0]};
-        if (!plan.uniform) {
-            ts_v.resize(2 * m);
-#pragma omp parallel for schedule(static)
-            for (int64_t s = 0; s < int64_t(2 * m); ++s) ts_v[s] = plan.tau[se[s]];
-            ts.v = ts_v.data();
-        }
-        E.upload_tau(ts);
-        lap("tau per slot");
-        double* d_g = static_cast<double*>(E.st->g_hat.ensure(sizeof(double) * 2 * m));
-        SABA_CUDA_CHECK(cudaMemsetAsync(d_g, 0, sizeof(double) * 2 * m, E.s));
-
-        // this shard's sources, batched by descending degree (tau~ correlates
-        // with degree; batching never changes a column's arithmetic)
-        std::vector<uint32_t> list;
-        const uint64_t total = sources ? source_count : n;
-        for (uint64_t i = shard_index; i < total; i += shard_count)
-            list.push_back(sources ? sources[i] : uint32_t(i));
-        std::stable_sort(list.begin(), list.end(),
-                         [&](uint32_t a, uint32_t b) { return E.deg(a) > E.deg(b); });
-        std::vector<uint32_t> tt_all(n, 0);
-        // Batches alternate between kWorkspaces workers, each with its own
-        // buffers, stream and host thread, so one batch's propagation
-        // overlaps another's walk phase. Sources write disjoint g_hat slots.
-        static const int workers_env = [] {  // SABA_AESC_WORKERS=1|2 overrides
-            const char* e = getenv("SABA_AESC_WORKERS");
-            return e ? std::max(1, std::min(kWorkspaces, atoi(e))) : 0;
-        }();
-        // (measured: 3 workers gain nothing on cfg3/cfg4; 2 beat 1 on cfg3 and,
-        // since the walk phase got cheaper, on the shallow cfg5 plan too: -11%)
-        const int nworkers = workers_env ? workers_env : (list.size() > size_t(kCols) ? kWorkspaces : 1);
-        std::vector<std::unique_ptr<Engine>> engines;
-        engines.emplace_back(new Engine(std::move(E)));
-        for (int w = 1; w < nworkers; ++w) {
-            engines.emplace_back(new Engine(g, w));
-            engines.back()->p = engines[0]->p;
-            engines.back()->upload_tau(ts);
-        }
-        SABA_CUDA_CHECK(cudaStreamSynchronize(engines[0]->s));  // g_hat zeroed before any batch
-        lap("workers ready");
-        std::vector<float> prop_ms(kWorkspaces, 0.f), walk_ms(kWorkspaces, 0.f);
-        std::vector<std::exception_ptr> failure(kWorkspaces);
-        const auto t0 = std::chrono::steady_clock::now();
-        auto worker = [&](int w) {
-            try {
-                SABA_CUDA_CHECK(cudaSetDevice(g->device));
-                Engine& W = *engines[w];
-                cudaEvent_t e0, e1, e2;
-                SABA_CUDA_CHECK(cudaEventCreate(&e0));
-                SABA_CUDA_CHECK(cudaEventCreate(&e1));
-                SABA_CUDA_CHECK(cudaEventCreate(&e2));
-                TileBuilder tb;
-                for (size_t b0 = size_t(w) * kCols; b0 < list.size(); b0 += size_t(nworkers) * kCols) {
-                    const std::vector<uint32_t> cols(list.begin() + b0,
-                                                     list.begin() + std::min(list.size(), b0 + kCols));
-                    const auto h0 = std::chrono::steady_clock::now();
-                    SABA_CUDA_CHECK(cudaEventRecord(e0, W.s));
-                    const std::vector<uint32_t> tt = W.propagate(cols, d_g);
-                    SABA_CUDA_CHECK(cudaEventRecord(e1, W.s));
-                    const auto h1 = std::chrono::steady_clock::now();
-                    tb.clear();
-                    for (size_t c = 0; c < cols.size(); ++c) {
-                        const uint32_t src = cols[c];
-                        tt_all[src] = tt[c];
-                        const uint32_t lo = g->h_off[src], hi = g->h_off[src + 1], deg_i = hi - lo;
-                        bool any = false;  // aesc.hpp:592-594
-                        for (uint32_t sl = lo; sl < hi && !any; ++sl) any = ts[sl] > tt[c];
-                        if (!any) continue;
-                        const uint64_t src_seed = substream(substream(cfg->master_seed, kAescTag), src);
-                        for (uint32_t sl = lo; sl < hi; ++sl) {
-                            const int64_t tau_eff = int64_t(ts[sl]) - int64_t(tt[c]);
-                            if (tau_eff <= 0) continue;
-                            const uint64_t n_req =
-                                walk_budget(uint32_t(tau_eff), cfg->epsilon, cfg->delta, deg_i, m);
-                            check_arg(cfg->switch_depth_cap < 0 ||
-                                          n_req * uint64_t(tau_eff) <= (uint64_t(1) << 26),
-                                      "aesc: walk budget infeasible (switch_depth_cap too aggressive for epsilon)");
-                            tb.add(sl, src, hadj[sl], uint32_t(tau_eff + 1), n_req, substream(src_seed, sl),
-                                   uint32_t(c));
-                            W.pairs += n_req;
-                            W.steps += 2 * n_req * uint64_t(tau_eff);
-                        }
-                    }
-                    // sparse supports: skip rho gathers of exact zeros via the bitmap
-                    static const int bitmap_mode = [] {  // 0 off, 1 on, 2 auto
-                        const char* e = getenv("SABA_AESC_BITMAP");
-                        return e ? atoi(e) : 2;
-                    }();
-                    // auto: supports of a few propagation steps are small even
-                    // when the batch's union frontier went dense
-                    const uint32_t tt_max = *std::max_element(tt.begin(), tt.end());
-                    const bool use_bits = bitmap_mode == 1 || (bitmap_mode == 2 && tt_max <= 4);
-                    const auto h2 = std::chrono::steady_clock::now();
-                    // the propagation above ended with a host sync, and run_tiles
-                    // returns after its own, so the two streams never overlap
-                    // within one worker
-                    run_tiles(g, W.st, W.st->stream_walk, tb, W.st->R.as<double>(),
-                              use_bits ? W.st->bits.as<uint32_t>() : nullptr, cfg->hash_multiplier,
-                              d_g, &W.launches);
-                    SABA_CUDA_CHECK(cudaEventRecord(e2, W.s));
-                    const auto h3 = std::chrono::steady_clock::now();
-                    W.clear_batch(int(cols.size()));
-                    SABA_CUDA_CHECK(cudaEventSynchronize(e2));
-                    float ta = 0.f, tw = 0.f;
-                    SABA_CUDA_CHECK(cudaEventElapsedTime(&ta, e0, e1));
-                    SABA_CUDA_CHECK(cudaEventElapsedTime(&tw, e1, e2));
-                    prop_ms[w] += ta;
-                    walk_ms[w] += tw;
-                    if (trace) {
-                        const auto h4 = std::chrono::steady_clock::now();
-                        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-                        fprintf(stderr, "[saba] aesc w%d batch %zu: propagate %.2f ms (device %.2f), tiles %.2f, "
-                                "run_tiles %.2f (device walk %.2f), clear+sync %.2f\n", w, b0 / kCols, ms(h0, h1), ta,
-                                ms(h1, h2), ms(h2, h3), tw, ms(h3, h4));
-                    }
-                }
-                SABA_CUDA_CHECK(cudaStreamSynchronize(W.s));
-                cudaEventDestroy(e0);
-                cudaEventDestroy(e1);
-                cudaEventDestroy(e2);
-            } catch (...) {
-                failure[w] = std::current_exception();
-            }
-        };
-        std::vector<std::thread> threads;
-        for (int w = 1; w < nworkers; ++w) threads.emplace_back(worker, w);
-        worker(0);
-        for (auto& t : threads) t.join();
-        for (auto& f : failure)
-            if (f) std::rethrow_exception(f);
-        lap("batches");
-        Engine& E0 = *engines[0];
-        for (int w = 1; w < nworkers; ++w) {
-            E0.pairs += engines[w]->pairs;
-            E0.steps += engines[w]->steps;
-            E0.launches += engines[w]->launches;
-            prop_ms[0] += prop_ms[w];
-            walk_ms[0] += walk_ms[w];
-        }
+        const auto t_out0 = std::chrono::steady_clock::now();
         if (full && s_hat_out) {
-            double* d_s = static_cast<double*>(E0.st->s_hat.ensure(sizeof(double) * m));
-            uint32_t* d_se = static_cast<uint32_t*>(E0.st->slot_edge_d.ensure(sizeof(uint32_t) * 2 * m));
-            copy_h2d(d_se, se, sizeof(uint32_t) * 2 * m, E0.s);
-            aesc_symmetrise<<<g->sm_count * 4, 256, 0, E0.s>>>(g->d_csr, g->d_adj, d_se, n, d_g, d_s);
-            SABA_CUDA_CHECK(cudaGetLastError());
-            ++E0.launches;
-            copy_d2h(s_hat_out, d_s, sizeof(double) * m, E0.s);
+            double* d_s = static_cast<double*>(root->aesc[0].s_hat.ensure(sizeof(double) * m, s));
+            enqueue_symmetrise(root, run.d_g[0], d_s, s);
+            ++run.launches;
+            copy_d2h(s_hat_out, d_s, sizeof(double) * m, s);
         }
-        copy_d2h(g_hat_out, d_g, sizeof(double) * 2 * m, E0.s);
-        lap("g_hat to host");
-        const auto t1 = std::chrono::steady_clock::now();
-        std::copy(plan.tau.begin(), plan.tau.end(), tau_out);
-        std::copy(tt_all.begin(), tt_all.end(), tau_tilde_out);
-        if (rep) {
-            saba_cu_aesc_report r{};
-            r.seconds = std::chrono::duration<double>(t1 - t0).count();
-            r.plan_seconds = std::chrono::duration<double>(t_plan1 - t_plan0).count();
-            r.propagation_ms = prop_ms[0];
-            r.walk_ms = walk_ms[0];
-            r.total_walk_pairs = E0.pairs;
-            r.total_walk_steps = E0.steps;
-            r.sources = list.size();
-            r.lambda_hat = plan.lambda_hat;
-            r.bipartite = plan.bipartite;
-            r.clamped = plan.clamped;
-            r.max_tau = plan.max_tau;
-            r.launches = E0.launches;
-            *rep = r;
-        }
+        copy_d2h(g_hat_out, run.d_g[0], sizeof(double) * 2 * m, s);
+        run.seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_out0).count();
+        std::copy(run.plan.tau.begin(), run.plan.tau.end(), tau_out);
+        std::copy(run.tt_all.begin(), run.tt_all.end(), tau_tilde_out);
+        if (rep) fill_aesc_report(run, rep);
+    });
+}
+
+int saba_cu_aesc_device(saba_cu_graph* g, const saba_cu_aesc_config* cfg, const uint32_t* sources,
+                        uint64_t source_count, uint32_t shard_index, uint32_t shard_count, double* g_hat_dev,
+                        uint32_t* tau_out, uint32_t* tau_tilde_out, void* stream, saba_cu_aesc_report* rep) {
+    return guard([&] {
+        check_arg(g && cfg && g_hat_dev, "null argument");
+        validate_cfg(*cfg);
+        check_arg(shard_count >= 1 && shard_index < shard_count, "bad shard index/count");
+        std::lock_guard<std::recursive_mutex> lock(g->mu);
+        DeviceScope scope(g->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        AescRun run;
+        aesc_run(g, *cfg, sources, source_count, shard_index, shard_count, false, run);
+        // the result is complete (aesc_run synchronised); the copy is ordered
+        // on the caller's stream like every later use of g_hat_dev
+        SABA_CUDA_CHECK(cudaMemcpyAsync(g_hat_dev, run.d_g[0], sizeof(double) * 2 * g->m,
+                                        cudaMemcpyDeviceToDevice, st));
+        SABA_CUDA_CHECK(cudaStreamSynchronize(st));  // run's workspace may be reused by the next call
+        if (tau_out) std::copy(run.plan.tau.begin(), run.plan.tau.end(), tau_out);
+        if (tau_tilde_out) std::copy(run.tt_all.begin(), run.tt_all.end(), tau_tilde_out);
+        if (rep) fill_aesc_report(run, rep);
+    });
+}
+
+int saba_cu_symmetrise(saba_cu_graph* g, const double* g_hat_dev, double* s_hat_dev, void* stream) {
+    return guard([&] {
+        check_arg(g && g_hat_dev && s_hat_dev, "null argument");
+        std::lock_guard<std::recursive_mutex> lock(g->mu);
+        DeviceScope scope(g->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        g->enter(st);
+        enqueue_symmetrise(g, g_hat_dev, s_hat_dev, st);
+        g->leave(st);
+    });
+}
+
+int saba_aesc_shard_sources(const uint32_t* offsets, uint32_t n, const uint32_t* sources,
+                            uint64_t source_count, uint32_t shard_index, uint32_t shard_count, uint32_t* out,
+                            uint64_t* out_count) {
+    return guard([&] {
+        check_arg(offsets && out_count, "null argument");
+        check_arg(source_count == 0 || sources, "null sources");
+        check_arg(shard_count >= 1 && shard_index < shard_count, "bad shard index/count");
+        const std::vector<uint32_t> mine =
+            shard_sources(offsets, n, sources, sources ? source_count : 0, shard_index, shard_count);
+        if (out) std::copy(mine.begin(), mine.end(), out);
+        *out_count = mine.size();
     });
 }
 
@@ -1799,6 +1966,7 @@ int saba_cu_propagate(saba_cu_graph* g, uint32_t source, const uint32_t* tau, do
     return guard([&] {
         check_arg(g && tau && prob_out && depth_out, "null argument");
         check_arg(source < g->n, "LandingPropagator: source out of range");
+        std::lock_guard<std::recursive_mutex> lock(g->mu);
         DeviceScope scope(g->device);
         const HostCsr h{g->n, g->m, g->h_off.data(), host_adj(g).data()};
         check_data(host_is_connected(h), "propagate_landing_probabilities: graph must be connected");
@@ -1836,6 +2004,7 @@ int saba_cu_estimate_edge(saba_cu_graph* g, uint32_t v_i, uint32_t v_j, const do
                   "cannot walk from an isolated vertex");
         check_arg(mode == SABA_MODE_HASH || mode == SABA_MODE_SABA, "mode not supported on GPU");
         check_arg(lanes >= 1 && lanes <= 64, "lanes must be in [1, 64]");
+        std::lock_guard<std::recursive_mutex> lock(g->mu);
         DeviceScope scope(g->device);
         Engine E(g);
         // dense rho = p / degree (aesc.hpp:541-548 uses the division form here)

@@ -32,6 +32,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
+#include <exception>
 
 #include "device_graph.cuh"
 #include "saba_hash.cuh"
@@ -621,8 +623,8 @@ uint64_t enqueue_campaign(saba_cu_graph* g, const saba_cu_campaign_config& c,
     uint32_t* kv = nullptr;
     uint64_t* off = nullptr;
     if (uniform_starts) {
-        kv = static_cast<uint32_t*>(g->kv.ensure(sizeof(uint32_t) * n));
-        off = static_cast<uint64_t*>(g->off.ensure(sizeof(uint64_t) * (size_t(n) + 1)));
+        kv = static_cast<uint32_t*>(g->kv.ensure(sizeof(uint32_t) * n, st));
+        off = static_cast<uint64_t*>(g->off.ensure(sizeof(uint64_t) * (size_t(n) + 1), st));
         SABA_CUDA_CHECK(cudaMemsetAsync(kv, 0, sizeof(uint32_t) * n, st));
         const uint64_t sstream = substream(c.master_seed, kStartTag);
         const int hb = int(std::min<uint64_t>((c.total_walks + 255) / 256, uint64_t(g->sm_count) * 16));
@@ -632,19 +634,19 @@ uint64_t enqueue_campaign(saba_cu_graph* g, const saba_cu_campaign_config& c,
         size_t tmp = 0;
         cub::TransformInputIterator<uint64_t, U32ToU64, const uint32_t*> it(kv, U32ToU64());
         SABA_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, it, off, int(n), st));
-        void* t = g->cub_tmp.ensure(tmp);
+        void* t = g->cub_tmp.ensure(tmp, st);
         SABA_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t, tmp, it, off, int(n), st));
         ++*launches;
     }
     const uint64_t chunk_cap = std::min<uint64_t>(kChunkWalks, r1 - r0 ? r1 - r0 : 1);
-    uint64_t* keys = static_cast<uint64_t*>(g->keys.ensure(sizeof(uint64_t) * chunk_cap));
+    uint64_t* keys = static_cast<uint64_t*>(g->keys.ensure(sizeof(uint64_t) * chunk_cap, st));
     uint64_t* keys_alt = c.mode == SABA_MODE_SABA
-                             ? static_cast<uint64_t*>(g->keys_alt.ensure(sizeof(uint64_t) * chunk_cap))
+                             ? static_cast<uint64_t*>(g->keys_alt.ensure(sizeof(uint64_t) * chunk_cap, st))
                              : nullptr;
-    int* seg = static_cast<int*>(g->seg.ensure(sizeof(int) * (size_t(n) + 1)));
+    int* seg = static_cast<int*>(g->seg.ensure(sizeof(int) * (size_t(n) + 1), st));
     // uint32 counters are exact when this launch's visits cannot reach 2^32
     const bool c32 = walk_variant().c32 && chunk_cap * c.length < (uint64_t(1) << 32);
-    uint32_t* counts32 = c32 ? static_cast<uint32_t*>(g->counts32.ensure(sizeof(uint32_t) * n)) : nullptr;
+    uint32_t* counts32 = c32 ? static_cast<uint32_t*>(g->counts32.ensure(sizeof(uint32_t) * n, st)) : nullptr;
     float total_walk_ms = 0.f;
     for (uint64_t a = r0; a < r1; a += chunk_cap) {
         const uint64_t b = std::min(r1, a + chunk_cap);
@@ -659,7 +661,7 @@ uint64_t enqueue_campaign(saba_cu_graph* g, const saba_cu_campaign_config& c,
             size_t tmp = 0;
             SABA_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, keys, keys_alt, int(nw),
                                                                int(n), seg, seg + 1, st));
-            void* t = g->cub_tmp.ensure(tmp);
+            void* t = g->cub_tmp.ensure(tmp, st);
             SABA_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(t, tmp, keys, keys_alt, int(nw), int(n),
                                                                seg, seg + 1, st));
             ++*launches;
@@ -721,21 +723,33 @@ int saba_cu_rng_stream(saba_cu_graph* g, const uint32_t* starts, uint32_t nstart
         }
         check_arg(selector == 1 || selector == 2,
                   "rng_stream: only the hashed selectors (xor, scaled) run on GPU");
+        check_arg(length == 1 || walks_per_vertex <= UINT64_MAX / (uint64_t(length) - 1) / nstarts,
+                  "rng_stream: nstarts * walks_per_vertex * (length - 1) overflows");
         *nwords = uint64_t(nstarts) * walks_per_vertex * (length - 1);
         if (length == 1) return;
         check_arg(words_out != nullptr, "null output");
+        std::lock_guard<std::recursive_mutex> lock(g->mu);
         DeviceScope scope(g->device);
+        // The stream feeds statistical test dumps that can be gigabytes long
+        // (stream.hpp:39-80 emits one start at a time): generate it in chunks
+        // of whole starts, at most ~256 MB of words per chunk (at least one
+        // start), each copied out before the next is generated.
+        const uint64_t per_start = walks_per_vertex * (length - 1);
+        const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(nstarts, (uint64_t(64) << 20) / per_start));
         DevBuf d_st, d_w;
         d_st.ensure(sizeof(uint32_t) * nstarts);
-        d_w.ensure(sizeof(uint32_t) * *nwords);
+        d_w.ensure(sizeof(uint32_t) * chunk * per_start);
         SABA_CUDA_CHECK(cudaMemcpy(d_st.p, starts, sizeof(uint32_t) * nstarts, cudaMemcpyHostToDevice));
-        const uint64_t total = uint64_t(nstarts) * walks_per_vertex;
-        const int blocks = int(std::min<uint64_t>((total + 255) / 256, uint64_t(g->sm_count) * 8));
-        rng_stream_kernel<<<blocks, 256>>>(g->d_csr, g->d_adj, d_st.as<uint32_t>(), total,
-                                           walks_per_vertex, length, master, mult, selector == 1,
-                                           d_w.as<uint32_t>());
-        SABA_CUDA_CHECK(cudaGetLastError());
-        SABA_CUDA_CHECK(cudaMemcpy(words_out, d_w.p, sizeof(uint32_t) * *nwords, cudaMemcpyDeviceToHost));
+        for (uint64_t s0 = 0; s0 < nstarts; s0 += chunk) {
+            const uint64_t ns = std::min<uint64_t>(chunk, nstarts - s0);
+            const uint64_t total = ns * walks_per_vertex;
+            const int blocks = int(std::min<uint64_t>((total + 255) / 256, uint64_t(g->sm_count) * 8));
+            rng_stream_kernel<<<blocks, 256>>>(g->d_csr, g->d_adj, d_st.as<uint32_t>() + s0, total,
+                                               walks_per_vertex, length, master, mult, selector == 1,
+                                               d_w.as<uint32_t>());
+            SABA_CUDA_CHECK(cudaGetLastError());
+            copy_d2h(words_out + s0 * per_start, d_w.p, sizeof(uint32_t) * ns * per_start, 0);
+        }
     });
 }
 
@@ -750,6 +764,7 @@ int saba_cu_walk_paths(saba_cu_graph* g, const uint32_t* starts, const uint32_t*
                       "cannot walk from an isolated vertex");
         }
         if (count == 0) return;
+        std::lock_guard<std::recursive_mutex> lock(g->mu);
         DeviceScope scope(g->device);
         DevBuf d_st, d_sd, d_p;
         d_st.ensure(sizeof(uint32_t) * count);
@@ -772,13 +787,16 @@ int saba_cu_walk_campaign_device(saba_cu_graph* g, const saba_cu_campaign_config
     return guard([&] {
         check_arg(g && cfg && counts_dev, "null argument");
         validate_campaign(g, *cfg);
+        std::lock_guard<std::recursive_mutex> lock(g->mu);
         DeviceScope scope(g->device);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         saba_cu_campaign_report r{};
         float walk_ms = 0.f;
+        g->enter(st);
         if (timing) SABA_CUDA_CHECK(cudaEventRecord(g->ev0, st));
         const uint64_t w = enqueue_campaign(g, *cfg, reinterpret_cast<unsigned long long*>(counts_dev),
                                             st, timing != 0, &walk_ms, &r.launches);
+        g->leave(st);
         if (timing) {
             SABA_CUDA_CHECK(cudaEventRecord(g->ev1, st));
             SABA_CUDA_CHECK(cudaEventSynchronize(g->ev1));
@@ -799,6 +817,7 @@ int saba_cu_branching_stats(saba_cu_graph* g, const saba_cu_campaign_config* cfg
         validate_campaign(g, *cfg);
         check_arg(cfg->length > 1, "branching statistics need walks of length > 1");
         check_arg(cfg->shard_count == 1, "branching statistics are computed unsharded");
+        std::lock_guard<std::recursive_mutex> lock(g->mu);
         DeviceScope scope(g->device);
         const uint32_t n = g->n, L = cfg->length, lanes = cfg->lanes;
         uint32_t* kv = nullptr;
@@ -844,23 +863,65 @@ int saba_cu_walk_campaign(saba_cu_graph* g, const saba_cu_campaign_config* cfg,
     return guard([&] {
         check_arg(g && cfg && counts_out, "null argument");
         validate_campaign(g, *cfg);
+        std::lock_guard<std::recursive_mutex> lock(g->mu);
+        // One shard per replica (a multi-device handle): replica r
+        // of R runs walk range shard_index * R + r of shard_count * R, which
+        // tile this call's range exactly; one host thread per replica, then
+        // one combine of the integer counts on the first replica.
+        const std::vector<saba_cu_graph*> reps = replicas_of(g);
+        const uint32_t R = uint32_t(reps.size());
+        std::vector<DevBuf> bufs(R);
+        std::vector<uint64_t> walks(R, 0);
+        std::vector<float> walk_ms(R, 0.f), span_ms(R, 0.f);
+        std::vector<uint32_t> launches(R, 0);
+        std::vector<std::exception_ptr> err(R);
+        const auto t0 = std::chrono::steady_clock::now();
+        auto run = [&](uint32_t r) {
+            try {
+                saba_cu_graph* h = reps[r];
+                std::unique_lock<std::recursive_mutex> lk(h->mu, std::defer_lock);
+                if (r) lk.lock();  // replica 0 is g, already held by this thread
+                DeviceScope scope(h->device);
+                saba_cu_campaign_config c = *cfg;
+                c.shard_index = cfg->shard_index * R + r;
+                c.shard_count = cfg->shard_count * R;
+                bufs[r].ensure(sizeof(uint64_t) * h->n, 0);
+                SABA_CUDA_CHECK(cudaMemsetAsync(bufs[r].p, 0, sizeof(uint64_t) * h->n, 0));
+                h->enter(0);
+                SABA_CUDA_CHECK(cudaEventRecord(h->ev0, 0));
+                walks[r] = enqueue_campaign(h, c, bufs[r].as<unsigned long long>(), 0, true, &walk_ms[r],
+                                            &launches[r]);
+                h->leave(0);
+                SABA_CUDA_CHECK(cudaEventRecord(h->ev1, 0));
+                SABA_CUDA_CHECK(cudaEventSynchronize(h->ev1));
+                SABA_CUDA_CHECK(cudaEventElapsedTime(&span_ms[r], h->ev0, h->ev1));
+            } catch (...) {
+                err[r] = std::current_exception();
+            }
+        };
+        std::vector<std::thread> threads;
+        for (uint32_t r = 1; r < R; ++r) threads.emplace_back(run, r);
+        run(0);
+        for (auto& t : threads) t.join();
+        for (auto& e : err)
+            if (e) std::rethrow_exception(e);
+        std::vector<void*> ptrs;
+        for (auto& b : bufs) ptrs.push_back(b.p);
+        reduce_to_root(reps, ptrs, g->n, ReduceType::U64, std::vector<cudaStream_t>(R, nullptr));
         DeviceScope scope(g->device);
-        DevBuf d_counts;
-        d_counts.ensure(sizeof(uint64_t) * g->n);
-        SABA_CUDA_CHECK(cudaMemsetAsync(d_counts.p, 0, sizeof(uint64_t) * g->n, 0));
+        SABA_CUDA_CHECK(cudaMemcpy(counts_out, bufs[0].p, sizeof(uint64_t) * g->n, cudaMemcpyDeviceToHost));
         saba_cu_campaign_report r{};
-        float walk_ms = 0.f;
-        SABA_CUDA_CHECK(cudaEventRecord(g->ev0, 0));
-        const uint64_t w = enqueue_campaign(g, *cfg, d_counts.as<unsigned long long>(), 0, true,
-                                            &walk_ms, &r.launches);
-        SABA_CUDA_CHECK(cudaEventRecord(g->ev1, 0));
-        SABA_CUDA_CHECK(cudaEventSynchronize(g->ev1));
-        float ms = 0.f;
-        SABA_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
-        r.seconds = ms * 1e-3;
-        r.walk_kernel_ms = walk_ms;
-        SABA_CUDA_CHECK(cudaMemcpy(counts_out, d_counts.p, sizeof(uint64_t) * g->n,
-                                   cudaMemcpyDeviceToHost));
+        if (R == 1) {
+            r.seconds = span_ms[0] * 1e-3;  // device events around the campaign
+        } else {
+            r.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+        uint64_t w = 0;
+        for (uint32_t i = 0; i < R; ++i) {
+            w += walks[i];
+            r.walk_kernel_ms = std::max(r.walk_kernel_ms, double(walk_ms[i]));
+            r.launches += launches[i];
+        }
         fill_report(g, *cfg, w, &r);
         if (rep) *rep = r;
     });

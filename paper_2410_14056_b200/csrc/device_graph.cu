@@ -106,6 +106,17 @@ void ensure_pool(int device) {
     done[device] = true;
 }
 
+void* pool_alloc_on(size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    ensure_pool(dev);
+    void* p = nullptr;
+    SABA_CUDA_CHECK(cudaMallocAsync(&p, bytes, s));
+    return p;
+}
+
+void pool_free_on(void* p, cudaStream_t s) { cudaFreeAsync(p, s); }
+
 void* pool_alloc(size_t bytes) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -281,7 +292,25 @@ const IdVec& slot_edges(saba_cu_graph* g) {
 
 }  // namespace saba_cu
 
+void saba_cu_graph::enter(cudaStream_t s) {
+    if (ev_use_recorded && last_stream != s) SABA_CUDA_CHECK(cudaStreamWaitEvent(s, ev_use, 0));
+}
+
+void saba_cu_graph::leave(cudaStream_t s) {
+    if (!ev_use) SABA_CUDA_CHECK(cudaEventCreateWithFlags(&ev_use, cudaEventDisableTiming));
+    SABA_CUDA_CHECK(cudaEventRecord(ev_use, s));
+    ev_use_recorded = true;
+    last_stream = s;
+}
+
 saba_cu_graph::~saba_cu_graph() {
+    for (saba_cu_graph* p : peers) {
+        saba_cu::DeviceScope scope(p->device);
+        delete p;
+    }
+    saba_cu::release_nccl(this);
+    cudaDeviceSynchronize();  // no kernel of an earlier asynchronous call may still read the replica
+    if (ev_use) cudaEventDestroy(ev_use);
     saba_cu::release_aesc_state(this);
     if (d_csr) saba_cu::pool_free(d_csr);
     if (d_adj) saba_cu::pool_free(d_adj);
@@ -312,10 +341,14 @@ int saba_cu_device_count(void) {
     return c;
 }
 
-int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uint32_t n,
-                         uint64_t two_m, int device, saba_cu_graph** out) {
-    return guard([&] {
-        check_arg(out != nullptr && offsets != nullptr, "null argument");
+}  // extern "C"
+
+namespace {
+saba_cu_graph* create_replica(const uint32_t* offsets, const uint32_t* adjacency, uint32_t n, uint64_t two_m,
+                              int device) {
+    saba_cu_graph* result = nullptr;
+    {
+        check_arg(offsets != nullptr, "null argument");
         check_arg(two_m == 0 || adjacency != nullptr, "null adjacency");
         check_data(n > 0, "empty graph");
         check_data(offsets[0] == 0 && offsets[n] == two_m && two_m % 2 == 0,
@@ -402,9 +435,35 @@ int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uin
         SABA_CUDA_CHECK(cudaEventCreate(&g->ev1));
         SABA_CUDA_CHECK(cudaEventCreate(&g->ev2));
         lap("events");
+        result = g.release();
+    }
+    return result;
+}
+}  // namespace
+
+extern "C" {
+
+int saba_cu_graph_create(const uint32_t* offsets, const uint32_t* adjacency, uint32_t n,
+                         uint64_t two_m, int device, saba_cu_graph** out) {
+    return guard([&] {
+        check_arg(out != nullptr, "null argument");
+        *out = create_replica(offsets, adjacency, n, two_m, device);
+    });
+}
+
+int saba_cu_graph_create_multi(const uint32_t* offsets, const uint32_t* adjacency, uint32_t n,
+                               uint64_t two_m, const int* devices, int ndev, saba_cu_graph** out) {
+    return guard([&] {
+        check_arg(out != nullptr && devices != nullptr, "null argument");
+        check_arg(ndev >= 1, "need at least one device");
+        std::unique_ptr<saba_cu_graph> g(create_replica(offsets, adjacency, n, two_m, devices[0]));
+        for (int i = 1; i < ndev; ++i)
+            g->peers.push_back(create_replica(offsets, adjacency, n, two_m, devices[i]));
         *out = g.release();
     });
 }
+
+int saba_cu_graph_replica_count(const saba_cu_graph* g) { return g ? 1 + int(g->peers.size()) : 0; }
 
 int saba_cu_graph_destroy(saba_cu_graph* g) {
     return guard([&] {

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "capi_util.hpp"
@@ -17,25 +18,52 @@ namespace saba_cu {
 // graph handle reuse the previous handle's memory instead of paying
 // cudaMalloc/cudaFree again (this is on the end-to-end path of every call).
 void ensure_pool(int device);
-void* pool_alloc(size_t bytes);
-void pool_free(void* p);
+void* pool_alloc(size_t bytes);                      // ready for any stream on return
+void* pool_alloc_on(size_t bytes, cudaStream_t s);  // stream-ordered: usable by work on s
+void pool_free(void* p);                             // ordered on the legacy stream
+void pool_free_on(void* p, cudaStream_t s);
 
-// Grow-only device buffer.
+// Grow-only device buffer. Growth is stream-ordered on the stream that will
+// use the buffer (ensure(b, s)): the old block is released after every
+// earlier operation on s and the new one is valid for work enqueued on s
+// afterwards. A handle's workspaces are only ever touched from one stream at
+// a time; entry points taking a caller stream first order that stream after
+// the handle's previous user (saba_cu_graph::enter), so a grow can never free
+// memory a kernel of an earlier call is still reading.
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    int dev = -1;  // device the block belongs to (freed there)
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() {
-        if (p) pool_free(p);
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), dev(o.dev) { o.p = nullptr; o.bytes = 0; }
+    ~DevBuf() { release(); }
+    void release() {
+        if (!p) return;
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (dev >= 0 && cur != dev) cudaSetDevice(dev);
+        pool_free(p);
+        if (dev >= 0 && cur != dev) cudaSetDevice(cur);
+        p = nullptr;
+        bytes = 0;
     }
     void* ensure(size_t b) {
         if (b <= bytes && p) return p;
-        if (p) pool_free(p);
+        release();
+        p = pool_alloc(b ? b : 1);
+        cudaGetDevice(&dev);
+        bytes = b;
+        return p;
+    }
+    void* ensure(size_t b, cudaStream_t s) {
+        if (b <= bytes && p) return p;
+        if (p) pool_free_on(p, s);
         p = nullptr;
         bytes = 0;
-        p = pool_alloc(b ? b : 1);
+        p = pool_alloc_on(b ? b : 1, s);
+        cudaGetDevice(&dev);
         bytes = b;
         return p;
     }
@@ -102,6 +130,25 @@ struct saba_cu_graph {
     saba_cu::DevBuf kv, off, keys, keys_alt, seg, cub_tmp, counts32;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     saba_cu::AescState* aesc = nullptr;  // owned; freed by release_aesc_state (aesc.cu)
+    // Every entry point holds `mu` for its whole call: the lazy builders
+    // (host adjacency, slot edges, fat / hot tables) and the workspaces above
+    // are shared state, and the reference's Graph allows unrestricted
+    // concurrent use (graph.hpp:24-27), so concurrent calls on one handle are
+    // serialised here instead of racing.
+    std::recursive_mutex mu;
+    // Stream chain of the asynchronous entry points: the stream of the last
+    // call and an event recorded at its end (see DevBuf).
+    cudaStream_t last_stream = nullptr;
+    cudaEvent_t ev_use = nullptr;
+    bool ev_use_recorded = false;
+    void enter(cudaStream_t s);  // order s after the previous user of the handle
+    void leave(cudaStream_t s);  // record this call's end on s
+    // Multi-device handle (saba_cu_graph_create_multi): the replicas on
+    // devices[1..ndev) (owned); this handle is the replica on devices[0].
+    // Entry points given such a handle run one shard per replica, one host
+    // thread each, and combine on this replica (multi_device.cu).
+    std::vector<saba_cu_graph*> peers;
+    void* nccl = nullptr;  // saba_cu::NcclGroup (multi_device.cu), created on first combine
     ~saba_cu_graph();
 };
 
@@ -115,6 +162,22 @@ bool ensure_fat16(saba_cu_graph* g);
 inline bool fat_fits_l2(const saba_cu_graph* g) { return 16 * g->m <= (uint64_t(48) << 20); }
 constexpr uint32_t kPackBits = 21;
 constexpr uint32_t kPackMax = 1u << kPackBits;  // ids must be < 2^21 to pack
+
+// Multi-device combine (multi_device.cu). replicas[0] is the root; bufs[r]
+// lives on replicas[r]'s device, `count` elements each, all zero outside the
+// slots that replica wrote. On return bufs[0] holds the element-wise sum
+// (exact: every element has at most one non-zero contributor for g_hat, and
+// integer sums for visit counts). An NCCL reduce over NVLink when the devices
+// are distinct and libnccl is loadable; otherwise (logical shards sharing a
+// device, or no NCCL) peer copies into the root plus an add kernel.
+enum class ReduceType { U64, F64 };
+void reduce_to_root(const std::vector<saba_cu_graph*>& replicas, const std::vector<void*>& bufs,
+                    size_t count, ReduceType type, const std::vector<cudaStream_t>& streams);
+// The replicas of a handle in shard order: {g, g->peers...}.
+std::vector<saba_cu_graph*> replicas_of(saba_cu_graph* g);
+// Name of the combine reduce_to_root used last ("nccl" / "peer"), for reports.
+const char* last_combine_kind();
+void release_nccl(saba_cu_graph* g);
 
 // Host <-> device copies of large caller-owned (pageable) buffers at PCIe
 // speed: through a pinned double-buffered staging ring with a parallel host

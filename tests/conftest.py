@@ -16,18 +16,9 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running full-size parity check")
 
 
-def _ensure_built():
-    lib = os.path.join(ROOT, "paper_2410_14056_b200", "libsaba_cuda.so")
-    if not os.path.exists(lib):
-        subprocess.run(["make", "-C", os.path.join(ROOT, "paper_2410_14056_b200", "csrc"), "-s",
-                        "-j8"], check=True, stdout=subprocess.DEVNULL)
-    orc = os.path.join(ROOT, "oracle", "_build", "liboracle.so")
-    if not os.path.exists(orc):
-        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-s", "oracle"], check=True,
-                       stdout=subprocess.DEVNULL)
+from __graft_entry__ import ensure_built  # noqa: E402
 
-
-_ensure_built()
+ensure_built()
 
 
 @pytest.fixture(scope="session")

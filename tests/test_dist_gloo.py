@@ -1,7 +1,8 @@
 """Multi-rank decomposition on CPU (gloo, world_size 2, 127.0.0.1).
 
 The GPU path shards (a) campaigns by contiguous ranges of the flattened
-(vertex, k) walk list and (b) AESC by interleaved sources, then combines with
+(vertex, k) walk list and (b) AESC by cost-stratified sources
+(saba_aesc_shard_sources: ascending degree, snake-dealt), then combines with
 one all-reduce. Here each rank evaluates its shard with the CPU
 oracle — the GPU kernels compute the same shards bit-exactly (see
 test_walks_gpu / test_aesc_gpu) — and the combine runs through
@@ -45,9 +46,9 @@ def _worker(rank, world, port, out_dir):
     part = O.campaign_range(g.offsets, g.adjacency, r0, r1, length=L, master=42, k_per_vertex=kv)
     t = torch.from_numpy(part.view(np.int64).copy())
     dist.all_reduce(t)
-    # (b) AESC: sources interleaved i % world == rank (aesc.cu)
+    # (b) AESC: cost-stratified source shards (aesc.cu shard_sources)
     src = np.arange(0, g.n, 7, dtype=np.uint32)
-    mine = sb.aesc_shard_sources(src, rank, world)
+    mine = sb.aesc_shard_sources(g, src, rank, world)
     est = O.aesc(g.offsets, g.adjacency, epsilon=0.1, delta=0.01, sources=mine, threads=1)
     gh = torch.from_numpy(est.g_hat.copy())
     dist.all_reduce(gh)
@@ -75,6 +76,18 @@ def test_shard_helpers_partition(sb):
             rs = [sb.campaign_shard_range(total, r, world) for r in range(world)]
             assert rs[0][0] == 0 and rs[-1][1] == total
             assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
-    src = np.arange(100, dtype=np.uint32)
-    parts = [sb.aesc_shard_sources(src, r, 3) for r in range(3)]
-    assert sorted(np.concatenate(parts).tolist()) == list(range(100))
+    g = sb.make_rmat(10, 8, seed=3)
+    src = np.arange(0, g.n, 3, dtype=np.uint32)
+    for world in (1, 2, 3, 8):
+        parts = [sb.aesc_shard_sources(g, src, r, world) for r in range(world)]
+        assert sorted(np.concatenate(parts).tolist()) == src.tolist()
+        # cost-stratified: every shard's degree profile is the same up to one source per class
+        if world > 1:
+            sums = [int(g.degrees()[p].sum()) for p in parts]
+            assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
+            assert max(sums) - min(sums) <= 2 * int(g.degrees().max())
+    # repeated sources run once (a repeat is idempotent in the reference's per-source loop)
+    rep = np.array([5, 5, 9, 1, 9], np.uint32)
+    assert sb.aesc_shard_sources(g, rep, 0, 1).tolist() == [1, 5, 9]
+    everything = sum(len(sb.aesc_shard_sources(g, None, r, 4)) for r in range(4))
+    assert everything == g.n

@@ -132,3 +132,15 @@ def test_aesc_source_subset_matches_full(golden, oracle):
     for s in src:
         sl = slice(off[s], off[s + 1])
         assert np.array_equal(r.g_hat[sl], full[sl])
+
+
+def test_oracle_generators_match_product(oracle, sb):
+    """oracle_gen.c (the generators the reference arm of bench.py uses, so that
+    it never loads the product library) builds the product's CSR bit for bit."""
+    cases = [(oracle.gen_rmat(12, 8, seed=7), sb.make_rmat(12, 8, seed=7)),
+             (oracle.gen_rmat(11, 4, seed=3, keep_lcc=False), sb.make_rmat(11, 4, seed=3, keep_lcc=False)),
+             (oracle.gen_erdos_renyi(4096, 16384, 1), sb.make_erdos_renyi(4096, 16384, 1)),
+             (oracle.gen_chung_lu(20000, 2.2, 12.0, 500.0, seed=4),
+              sb.make_chung_lu(20000, 2.2, 12.0, 500.0, seed=4))]
+    for (off, adj), g in cases:
+        assert np.array_equal(off, g.offsets) and np.array_equal(adj, g.adjacency)
