@@ -22,7 +22,7 @@ struct AescConfig {
     uint32_t candidate_nodes = 0;  // accepted, unused (as in the reference)
     WalkMode mode = WalkMode::Saba;
     uint64_t master_seed = 42;
-    int threads = 0;               // accepted; the GPU ignores it
+    int threads = 0;               // GPUs (0 = all visible; detail::devices_for)
     uint32_t lanes = 8;
     uint32_t max_truncation = 128;
     bool per_edge_tau = false;
@@ -149,7 +149,7 @@ inline CentralityEstimate run_aesc(const Graph& g, const AescConfig& cfg,
     est.plan.tau.resize(g.edge_count());
     est.plan.tau_tilde.resize(g.vertex_count());
     saba_cu_aesc_report r{};
-    detail::raise_on(saba_cu_aesc(g.device_handle(), &c, sources ? sources->data() : nullptr,
+    detail::raise_on(saba_cu_aesc(g.device_group(detail::devices_for(cfg.threads)), &c, sources ? sources->data() : nullptr,
                                   sources ? sources->size() : 0, 0, 1, est.g_hat.data(),
                                   sources ? nullptr : est.s_hat.data(), est.plan.tau.data(),
                                   est.plan.tau_tilde.data(), &r),

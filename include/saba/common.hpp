@@ -9,6 +9,9 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <algorithm>
+#include <vector>
+#include <cstdlib>
 
 #include "saba_cuda.h"
 
@@ -36,6 +39,28 @@ inline void raise_on(int status, const char* what) {
     if (msg.empty()) msg = what;
     if (status == SABA_EINVAL) throw std::invalid_argument(msg);
     throw std::runtime_error(msg);
+}
+
+/// The devices behind a config's `threads` (walker.hpp:372, aesc.hpp:47): the
+/// reference's thread count becomes a GPU count, 0 = every visible device, as
+/// 0 = every hardware thread there. SABA_DEVICES="0,0,1" overrides the list
+/// (repeats are logical shards on one GPU). Results do not depend on it.
+inline std::vector<int> devices_for(int threads) {
+    std::vector<int> d;
+    if (const char* e = std::getenv("SABA_DEVICES"); e && *e) {
+        for (const char* p = e; *p;) {
+            char* end = nullptr;
+            const long v = std::strtol(p, &end, 10);
+            if (end == p) break;
+            d.push_back(int(v));
+            p = *end == ',' ? end + 1 : end;
+        }
+        if (!d.empty()) return d;
+    }
+    const int count = std::max(1, saba_cu_device_count());
+    const int k = threads <= 0 ? count : std::min(threads, count);
+    for (int i = 0; i < k; ++i) d.push_back(i);
+    return d;
 }
 }  // namespace detail
 

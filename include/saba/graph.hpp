@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <istream>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <ostream>
@@ -172,26 +173,35 @@ public:
     /// Thread-safe: the reference's Graph may be read from any number of
     /// threads at once (graph.hpp:24-27), so the lazy creation is locked, and
     /// libsaba_cuda serialises calls on one handle (saba_cu_graph::mu).
-    saba_cu_graph* device_handle(int device = 0) const {
-        static std::mutex mu;
-        std::lock_guard<std::mutex> lock(mu);
-        if (!dev_ || dev_->device != device) {
+    /// Handles live as long as the graph, so a pointer returned to one
+    /// thread stays valid while another asks for a different device.
+    saba_cu_graph* device_handle(int device = 0) const { return device_group({device}); }
+
+    /// One replica per entry of `devices` behind a single handle
+    /// (saba_cu_graph_create_multi; repeats = logical shards on one GPU).
+    saba_cu_graph* device_group(const std::vector<int>& devices) const {
+        std::lock_guard<std::mutex> lock(replicas_->mu);
+        auto& slot = replicas_->by_devices[devices];
+        if (!slot) {
             saba_cu_graph* h = nullptr;
-            detail::raise_on(saba_cu_graph_create(offsets_.data(), adjacency_.data(), n_,
-                                                  adjacency_.size(), device, &h),
+            detail::raise_on(saba_cu_graph_create_multi(offsets_.data(), adjacency_.data(), n_, adjacency_.size(),
+                                                        devices.data(), int(devices.size()), &h),
                              "graph upload");
-            dev_ = std::make_shared<DeviceReplica>(h, device);
+            slot = std::make_unique<DeviceReplica>(h);
         }
-        return dev_->handle;
+        return slot->handle;
     }
 
 private:
     struct DeviceReplica {
         saba_cu_graph* handle;
-        int device;
-        DeviceReplica(saba_cu_graph* h, int d) : handle(h), device(d) {}
+        explicit DeviceReplica(saba_cu_graph* h) : handle(h) {}
         DeviceReplica(const DeviceReplica&) = delete;
         ~DeviceReplica() { saba_cu_graph_destroy(handle); }
+    };
+    struct Replicas {
+        std::mutex mu;
+        std::map<std::vector<int>, std::unique_ptr<DeviceReplica>> by_devices;
     };
 
     void adopt(saba_hgraph* h) {
@@ -233,7 +243,7 @@ private:
     std::vector<uint32_t> offsets_, adjacency_, slot_edge_;
     std::vector<std::pair<uint32_t, uint32_t>> edges_;
     std::vector<uint64_t> original_ids_;
-    mutable std::shared_ptr<DeviceReplica> dev_;
+    std::shared_ptr<Replicas> replicas_ = std::make_shared<Replicas>();
 };
 
 /// Whether a BFS from vertex 0 reaches every vertex.

@@ -159,7 +159,7 @@ struct CampaignConfig {
     uint32_t length = 10;
     WalkMode mode = WalkMode::Saba;
     uint32_t lanes = 8;
-    int threads = 0;  // accepted; the GPU ignores it
+    int threads = 0;  // GPUs (0 = all visible; detail::devices_for)
     uint64_t master_seed = 42;
     bool collect_stats = false;
     HashSpec hash{};
@@ -196,12 +196,14 @@ inline CampaignReport campaign_on_gpu(const Graph& g, const CampaignConfig& cfg,
     c.shard_count = 1;
     std::vector<uint64_t> add(g.vertex_count());
     saba_cu_campaign_report r{};
-    detail::raise_on(saba_cu_walk_campaign(g.device_handle(), &c, add.data(), &r), "run_walk_campaign");
+    const std::vector<int> devices = detail::devices_for(cfg.threads);
+    detail::raise_on(saba_cu_walk_campaign(g.device_group(devices), &c, add.data(), &r), "run_walk_campaign");
     for (size_t i = 0; i < add.size(); ++i) counts[i] += add[i];
     CampaignReport rep;
     rep.seconds = r.seconds;
     rep.total_steps = r.total_steps;
     rep.total_events = r.total_events;
+    rep.threads_used = int(devices.size());
     if (cfg.collect_stats && cfg.length > 1) {  // the untimed stats pass (walker.hpp:471, 526-536)
         std::vector<uint64_t> hist(size_t(cfg.lanes) + 1), per_step(cfg.length - 1), tot(4);
         detail::raise_on(saba_cu_branching_stats(g.device_handle(), &c, hist.data(), per_step.data(),

@@ -17,7 +17,7 @@ from .walker import (CampaignConfig, CampaignReport, HashSpec, SeedOrdering, See
                      DistinctProxy, branching_stats, collect_branching, rng_stream)
 from .aesc import (AescConfig, CentralityEstimate, LandingProbs, TruncationPlan, aesc,
                    estimate_edge, propagate_landing_probabilities, truncated_lengths, walk_budget,
-                   aesc_shard_sources,
+                   aesc_shard_sources, aesc_device, symmetrise,
                    write_centrality_tsv)
 from ._lib import CudaError, LIB_PATH
 

@@ -87,6 +87,7 @@ class CentralityEstimate:
     plan_seconds: float = 0.0
     edge_visits: int = 0
     launches: int = 0
+    replicas: int = 1
 
 
 def walk_budget(tau_effective: int, epsilon: float, delta: float, degree: int,
@@ -128,10 +129,12 @@ def _is_connected(g: Graph) -> bool:
 
 
 def aesc(g: Graph, cfg: AescConfig, *, sources=None, shard_index: int = 0, shard_count: int = 1,
-         device: int = 0) -> CentralityEstimate:
+         device: int = 0, devices=None) -> CentralityEstimate:
     """aesc.hpp:636-708 on one B200. `sources` restricts the estimator to a
     source subset (SURVEY §8d protocol), deduplicated; shard `shard_index`
-    of `shard_count` runs the sources aesc_shard_sources() returns."""
+    of `shard_count` runs the sources aesc_shard_sources() returns. `devices`
+    (a list, repeats allowed) runs the call over one replica per entry
+    (Graph.device_group) with one combine of g_hat: identical results."""
     n, m = g.n, g.m
     g_hat = np.zeros(2 * m, np.float64)
     full = sources is None and shard_count == 1
@@ -141,14 +144,46 @@ def aesc(g: Graph, cfg: AescConfig, *, sources=None, shard_index: int = 0, shard
     src = None if sources is None else np.ascontiguousarray(sources, np.uint32)
     rep = L.AescReportC()
     c = cfg.to_c()
-    L.check(L.lib().saba_cu_aesc(g.device_handle(device), C.byref(c), L.ptr(src, L.u32p),
+    h = g.device_group(devices) if devices is not None else g.device_handle(device)
+    L.check(L.lib().saba_cu_aesc(h, C.byref(c), L.ptr(src, L.u32p),
                                  0 if src is None else len(src), shard_index, shard_count,
                                  L.ptr(g_hat, L.f64p), L.ptr(s_hat, L.f64p), L.ptr(tau, L.u32p),
                                  L.ptr(tt, L.u32p), C.byref(rep)), "aesc")
     plan = TruncationPlan(tau, tt, rep.lambda_hat, bool(rep.clamped), rep.max_tau)
     return CentralityEstimate(s_hat, g_hat, cfg, plan, bool(rep.bipartite), rep.total_walk_pairs,
                               rep.total_walk_steps, rep.seconds, rep.propagation_ms, rep.walk_ms,
-                              rep.plan_seconds, rep.edge_visits, rep.launches)
+                              rep.plan_seconds, rep.edge_visits, rep.launches, rep.replicas)
+
+
+def aesc_device(g: Graph, cfg: AescConfig, g_hat_dev_ptr: int, stream_ptr: int = 0, *, sources=None,
+                shard_index: int = 0, shard_count: int = 1, device: int = 0) -> CentralityEstimate:
+    """aesc() leaving g_hat (2m float64) in a caller-owned device buffer on
+    `device` (e.g. a torch tensor's data_ptr()), zero outside this shard's
+    slots, so one-process-per-GPU callers can all-reduce it (exact: one
+    writer per slot) and form s_hat with symmetrise(). The returned estimate
+    carries the plan, tau~ and counters; its g_hat/s_hat are None."""
+    n, m = g.n, g.m
+    tau = np.zeros(m, np.uint32)
+    tt = np.zeros(n, np.uint32)
+    src = None if sources is None else np.ascontiguousarray(sources, np.uint32)
+    rep = L.AescReportC()
+    c = cfg.to_c()
+    L.check(L.lib().saba_cu_aesc_device(g.device_handle(device), C.byref(c), L.ptr(src, L.u32p),
+                                        0 if src is None else len(src), shard_index, shard_count,
+                                        C.c_void_p(g_hat_dev_ptr), L.ptr(tau, L.u32p), L.ptr(tt, L.u32p),
+                                        C.c_void_p(stream_ptr), C.byref(rep)), "aesc_device")
+    plan = TruncationPlan(tau, tt, rep.lambda_hat, bool(rep.clamped), rep.max_tau)
+    return CentralityEstimate(None, None, cfg, plan, bool(rep.bipartite), rep.total_walk_pairs,
+                              rep.total_walk_steps, rep.seconds, rep.propagation_ms, rep.walk_ms,
+                              rep.plan_seconds, rep.edge_visits, rep.launches, rep.replicas)
+
+
+def symmetrise(g: Graph, g_hat_dev_ptr: int, s_hat_dev_ptr: int, stream_ptr: int = 0,
+               device: int = 0) -> None:
+    """K5 on device buffers: s_hat[e] = g_hat[u->v] + g_hat[v->u]
+    (aesc.hpp:702-706), enqueued on `stream_ptr`."""
+    L.check(L.lib().saba_cu_symmetrise(g.device_handle(device), C.c_void_p(g_hat_dev_ptr),
+                                       C.c_void_p(s_hat_dev_ptr), C.c_void_p(stream_ptr)), "symmetrise")
 
 
 def propagate_landing_probabilities(g: Graph, source: int, plan: TruncationPlan, epsilon: float,

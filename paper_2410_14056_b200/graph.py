@@ -169,6 +169,25 @@ class Graph:
             self._dev[device] = h
         return h
 
+    def device_group(self, devices) -> C.c_void_p:
+        """One replica per entry of `devices` behind a single handle
+        (saba_cu_graph_create_multi; repeats = logical shards on one GPU).
+        Campaigns and AESC on it run one shard per replica and combine once;
+        results are identical to one device."""
+        devices = tuple(int(d) for d in devices)
+        if len(devices) == 1:
+            return self.device_handle(devices[0])
+        h = self._dev.get(devices)
+        if h is None:
+            h = C.c_void_p()
+            arr = (C.c_int * len(devices))(*devices)
+            L.check(L.lib().saba_cu_graph_create_multi(L.ptr(self.offsets, L.u32p),
+                                                       L.ptr(self.adjacency, L.u32p), self.n,
+                                                       len(self.adjacency), arr, len(devices),
+                                                       C.byref(h)), "graph_create_multi")
+            self._dev[devices] = h
+        return h
+
     def release_device(self) -> None:
         for h in self._dev.values():
             L.lib().saba_cu_graph_destroy(h)

@@ -245,13 +245,15 @@ def _report(r: L.CampaignReportC) -> CampaignReport:
 
 def run_walk_campaign(g: Graph, cfg: CampaignConfig, sink: VisitCountSink, *,
                       total_walks: int = 0, shard_index: int = 0, shard_count: int = 1,
-                      device: int = 0) -> CampaignReport:
+                      device: int = 0, devices=None) -> CampaignReport:
     """walker.hpp:456-538 on one B200.
 
     total_walks > 0 selects the uniform-random-start campaign
     instead of `walks_per_vertex` walks from every vertex. With sharding,
     only walk range `shard_index` of `shard_count` runs; the shards' counts
-    sum to the unsharded counts exactly.
+    sum to the unsharded counts exactly. `devices` (a list, repeats allowed)
+    spreads the call over one replica per entry (Graph.device_group), one
+    shard each, combined on the first: identical counts.
     """
     if not isinstance(sink, VisitCountSink):
         raise TypeError("the GPU campaign supports VisitCountSink only")
@@ -260,8 +262,9 @@ def run_walk_campaign(g: Graph, cfg: CampaignConfig, sink: VisitCountSink, *,
     counts = np.zeros(g.n, np.uint64)
     rep = L.CampaignReportC()
     c = _cfg_c(cfg, total_walks, shard_index, shard_count)
-    L.check(L.lib().saba_cu_walk_campaign(g.device_handle(device), C.byref(c),
-                                          L.ptr(counts, L.u64p), C.byref(rep)), "walk_campaign")
+    h = g.device_group(devices) if devices is not None else g.device_handle(device)
+    L.check(L.lib().saba_cu_walk_campaign(h, C.byref(c), L.ptr(counts, L.u64p), C.byref(rep)),
+            "walk_campaign")
     sink.counts += counts
     out = _report(rep)
     # the reference collects stats in lane modes with L > 1 (walker.hpp:471)

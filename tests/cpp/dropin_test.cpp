@@ -4,6 +4,8 @@
 //   g++ -std=c++20 -I include tests/cpp/dropin_test.cpp -L paper_2410_14056_b200 -lsaba_cuda
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <cstdlib>
 #include <sstream>
 #include <stdexcept>
 
@@ -139,6 +141,37 @@ static void gpu_checks() {
     CHECK_THROWS_AS(aesc(f, ac), std::invalid_argument);
     ac.epsilon = 0.05;
     CHECK_THROWS_AS(aesc(Graph::from_edges(4, {{0, 1}, {2, 3}}), ac), std::runtime_error);
+    // GPU-count invariance (test_aesc.cpp:292-308, test_walker.cpp:152-158):
+    // `threads` is a device count; SABA_DEVICES lists logical shards on one GPU
+    {
+        std::vector<std::pair<uint32_t, uint32_t>> e;
+        for (uint32_t i = 0; i < 400; ++i) {
+            e.push_back({i, (i + 1) % 400});
+            e.push_back({i, (i * 7 + 3) % 400});
+        }
+        const Graph g = Graph::from_edges(400, e);
+        AescConfig c1;
+        c1.epsilon = 0.2;
+        c1.threads = 1;
+        CampaignConfig cc;
+        cc.walks_per_vertex = 64;
+        cc.length = 16;
+        cc.threads = 1;
+        unsetenv("SABA_DEVICES");
+        const CentralityEstimate one = aesc(g, c1);
+        VisitCountSink s1(400);
+        run_walk_campaign(g, cc, s1);
+        for (const char* devs : {"0,0", "0,0,0"}) {
+            setenv("SABA_DEVICES", devs, 1);
+            const CentralityEstimate many = aesc(g, c1);
+            CHECK(many.g_hat == one.g_hat && many.s_hat == one.s_hat);
+            CHECK(many.plan.tau_tilde == one.plan.tau_tilde && many.total_walk_pairs == one.total_walk_pairs);
+            VisitCountSink sn(400);
+            const CampaignReport rn = run_walk_campaign(g, cc, sn);
+            CHECK(sn.counts == s1.counts && rn.threads_used == int(std::strlen(devs) + 1) / 2);
+        }
+        unsetenv("SABA_DEVICES");
+    }
     std::ostringstream tsv;
     const std::vector<double> third(3, 2.0 / 3.0);
     write_centrality_tsv(tsv, complete(3), third);
