@@ -88,6 +88,7 @@ struct AescState {
     DevBuf heavy_rows, piece_off, pieces, part, part_mask;  // hub-row split (static per graph)
     uint32_t nheavy = 0, npieces = 0;
     DevBuf light_order;  // light rows by descending degree (dense depths)
+    DevBuf recs;         // per-vertex walk records of the batch's columns (aesc_walk_rec)
     uint32_t nlight = 0;
     bool heavy_built = false;
     cudaStream_t stream = nullptr;       // propagation (and everything else)
@@ -850,6 +851,7 @@ __global__ void __launch_bounds__(256, MINB)
                      const uint32_t* __restrict__ bits, uint32_t words, uint64_t mult,
                      const uint64_t* __restrict__ fat, uint32_t fat_idb, uint32_t fat_sh,
                      const uint4* __restrict__ fat16, double* __restrict__ score) {
+
     // Software-pipelined score side: the walk chain (csr -> adj, or one fat
     // gather) is the only dependency carried from step to step; the support
     // bit of x_l is loaded right after x_l is known, the rho gather of x_l is
@@ -932,6 +934,88 @@ __global__ void __launch_bounds__(256, MINB)
         }
 #pragma unroll
         for (int r = 0; r < WPT; ++r) {  // walk ids are re-read (one register less per walk)
+            const uint64_t e = base + uint64_t(r) * 32 + lane;
+            if (e < nwalks) score[vals[e]] = sc[r];
+        }
+    }
+}
+
+// Per-vertex walk records of one batch (beyond-L2 graphs): column c's
+// record of vertex v is {base, degree, rho_c(v)} in 16 B, so the step from
+// x_{l-1} loads ONE record that carries both what the selection needs and the
+// score term of x_{l-1} (aesc.hpp:491-493) — two dependent gathers per step
+// (record, neighbour id) instead of three (csr, neighbour id, rho). rho_c is
+// exact zero outside column c's support, as in R.
+__global__ void aesc_build_records(const uint2* __restrict__ csr, const double* __restrict__ R, uint32_t n,
+                                   uint32_t ncols, uint4* __restrict__ recs) {
+    const uint64_t total = uint64_t(ncols) * n;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t v = uint32_t(i % n);
+        const uint2 r = csr[v];
+        const double rho = __ldcs(R + i);
+        recs[i] = make_uint4(r.x, r.y, uint32_t(__double_as_longlong(rho)),
+                             uint32_t(uint64_t(__double_as_longlong(rho)) >> 32));
+    }
+}
+
+// K4 over per-vertex records (see aesc_build_records). Same walks, same
+// seeds, same step-order score sum as aesc_walk_sorted: the record loaded to
+// leave x_{l-1} adds rho(x_{l-1}) for l >= 2, and x_{len-1}'s record is
+// loaded once after the loop.
+template <bool PACKED, int WPT, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    aesc_walk_rec(const uint32_t* __restrict__ gidx, const uint32_t* __restrict__ vals, uint32_t nwalks,
+                  const WalkGroup* __restrict__ groups, const uint4* __restrict__ recs,
+                  const uint32_t* __restrict__ adj, const uint64_t* __restrict__ adjp, uint32_t n, uint64_t mult,
+                  double* __restrict__ score) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint64_t base = uint64_t(warp) * 32 * WPT; base < nwalks; base += uint64_t(nwarps) * 32 * WPT) {
+        uint32_t cur[WPT], seed[WPT], len[WPT], col[WPT];  // col = column * n (< 2^32, host-checked)
+        double sc[WPT];
+        uint32_t maxlen = 1;
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {
+            const uint64_t e = base + uint64_t(r) * 32 + lane;
+            len[r] = 1;
+            sc[r] = 0.0;
+            cur[r] = 0;
+            seed[r] = 0;
+            col[r] = 0;
+            if (e < nwalks) {
+                const uint32_t w = vals[e];
+                const WalkGroup G = groups[gidx[e]];
+                const uint32_t local = w - G.walk_off;
+                const uint32_t side = local >= G.pairs;
+                seed[r] = walk_seed(G.edge_seed, 2 * (G.k0 + (local - side * G.pairs)) + side);
+                cur[r] = side ? G.vj : G.vi;
+                len[r] = G.len;
+                col[r] = G.col * n;
+            }
+            maxlen = max(maxlen, len[r]);
+        }
+        maxlen = __reduce_max_sync(0xffffffffu, maxlen);
+        for (uint32_t l = 1; l < maxlen; ++l) {
+            uint4 q[WPT];
+#pragma unroll
+            for (int r = 0; r < WPT; ++r)
+                if (l < len[r]) q[r] = __ldg(recs + (col[r] + cur[r]));
+#pragma unroll
+            for (int r = 0; r < WPT; ++r)
+                if (l < len[r]) {
+                    if (l >= 2) sc[r] += __hiloint2double(int(q[r].w), int(q[r].z));  // rho(x_{l-1})
+                    const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
+                    cur[r] = adj_at<PACKED>(adj, adjp, q[r].x + scaled_index(raw, q[r].y));
+                }
+        }
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {
+            if (len[r] > 1) {  // rho(x_{len-1})
+                const uint4 q = __ldg(recs + (col[r] + cur[r]));
+                sc[r] += __hiloint2double(int(q.w), int(q.z));
+            }
             const uint64_t e = base + uint64_t(r) * 32 + lane;
             if (e < nwalks) score[vals[e]] = sc[r];
         }
@@ -1335,6 +1419,17 @@ bool aesc_fat_enabled() {  // SABA_AESC_FAT=0 disables (default: on when L2-resi
     return on;
 }
 
+// Per-vertex records (aesc_walk_rec): 1 = on for the compact path (graphs
+// beyond L2 without 16-byte slot records), 0 = off, 2 = for every batch
+// (tuning knob SABA_AESC_REC).
+int aesc_rec_mode() {
+    static const int m = [] {
+        const char* e = getenv("SABA_AESC_REC");
+        return e ? atoi(e) : 1;
+    }();
+    return m;
+}
+
 // K4s host side: segments of the chunk, coarse tiles and the coarse-bucket
 // table (a segment up to kFineDirect walks is one bucket), then count ->
 // exclusive scan -> scatter -> fine bucketing into (out_w, out_g).
@@ -1415,6 +1510,7 @@ struct Launch {
     uint64_t mult;
     double* score;
     cudaStream_t s;
+    const uint4* recs;  // per-vertex records of the batch (aesc_walk_rec), or null
 };
 
 template <bool P, int WPT, bool B, bool F, int MINB, bool F16 = false>
@@ -1429,8 +1525,23 @@ void walk_launch(const Launch& L) {
                              L.g->d_adj_fat16, L.score);
 }
 
+template <bool P, int WPT, int MINB>
+void rec_launch(const Launch& L) {
+    auto k = aesc_walk_rec<P, WPT, MINB>;
+    int occ = 0;
+    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0));
+    const int grid = int(std::min<uint64_t>((uint64_t(L.nw) + 32 * WPT - 1) / (32 * WPT) * 32 / 256 + 1,
+                                            uint64_t(L.g->sm_count) * std::max(occ, 1)));
+    k<<<grid, 256, 0, L.s>>>(L.out_g, L.out_w, L.nw, L.dg, L.recs, L.g->d_adj, L.g->d_adj_packed, L.g->n, L.mult,
+                             L.score);
+}
+
 template <int WPT, int MINB>
 void walk_dispatch(const Launch& L, bool fat, bool packed, bool f16) {
+    if (L.recs) {
+        if (packed) rec_launch<true, WPT, MINB>(L); else rec_launch<false, WPT, MINB>(L);
+        return;
+    }
     const bool b = L.bits != nullptr;
     if (f16) {
         if (b) walk_launch<false, WPT, true, false, MINB, true>(L); else walk_launch<false, WPT, false, false, MINB, true>(L);
@@ -1444,7 +1555,8 @@ void walk_dispatch(const Launch& L, bool fat, bool packed, bool f16) {
 }
 
 void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb, const double* R,
-               const uint32_t* bits, uint64_t mult, double* g_hat_dev, uint32_t* launches) {
+               const uint32_t* bits, uint64_t mult, double* g_hat_dev, uint32_t* launches,
+               const uint4* recs = nullptr) {
     const uint32_t words = (g->n + 31) / 32;
     if (tb.empty()) return;
     double* part = static_cast<double*>(st->partials.ensure(sizeof(double) * std::max(tb.ntiles, 1u)));
@@ -1472,7 +1584,7 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
             return e ? uint64_t(atoi(e)) : uint64_t(kShortWalk);
         }();
         const bool short_walks = c.steps < short_steps * nw;
-        const Launch L{out_g, out_w, nw, dg, g, R, bits, words, mult, score, s};
+        const Launch L{out_g, out_w, nw, dg, g, R, bits, words, mult, score, s, recs};
         if (short_walks)
             walk_dispatch<kShortWpt, kShortMinb>(L, fat, packed, f16);
         else
@@ -1800,8 +1912,25 @@ void aesc_run(saba_cu_graph* g, const saba_cu_aesc_config& cfg, const uint32_t* 
                 // the propagation above ended with a host sync, and run_tiles
                 // returns after its own, so the two streams never overlap
                 // within one worker
+                const bool fat_path = rg->d_adj_fat != nullptr && fat_fits_l2(rg) && aesc_fat_enabled();
+                const bool f16_path = !fat_path && rg->d_adj_fat16 != nullptr && aesc_fat16_enabled();
+                const int rec_mode = aesc_rec_mode();
+                const bool use_rec = !tb.empty() && (rec_mode == 2 || (rec_mode == 1 && !fat_path && !f16_path));
+                const uint4* recs = nullptr;
+                if (use_rec) {
+                    cudaStream_t ws = W.st->stream_walk;
+                    uint4* rb = static_cast<uint4*>(W.st->recs.ensure(sizeof(uint4) * size_t(n) * cols.size(), ws));
+                    const uint64_t total = uint64_t(n) * cols.size();
+                    const int grid = int(std::min<uint64_t>((total + 255) / 256, uint64_t(rg->sm_count) * 16));
+                    aesc_build_records<<<grid, 256, 0, ws>>>(rg->d_csr, W.st->R.as<double>(), n,
+                                                             uint32_t(cols.size()), rb);
+                    SABA_CUDA_CHECK(cudaGetLastError());
+                    ++W.launches;
+                    recs = rb;
+                }
                 run_tiles(rg, W.st, W.st->stream_walk, tb, W.st->R.as<double>(),
-                          use_bits ? W.st->bits.as<uint32_t>() : nullptr, cfg.hash_multiplier, d_g, &W.launches);
+                          use_bits && !use_rec ? W.st->bits.as<uint32_t>() : nullptr, cfg.hash_multiplier, d_g,
+                          &W.launches, recs);
                 SABA_CUDA_CHECK(cudaEventRecord(e2, W.s));
                 const auto h3 = std::chrono::steady_clock::now();
                 W.clear_batch(int(cols.size()));

@@ -116,3 +116,33 @@ def test_device_campaign_across_streams_with_growing_workspace(sb):
         torch.cuda.synchronize()
         assert np.array_equal(a.cpu().numpy().astype(np.uint64), want_small.counts)
         assert np.array_equal(b.cpu().numpy().astype(np.uint64), want_big.counts)
+
+
+def test_bench_two_ranks_gloo_on_one_gpu(oracle):
+    """bench.py's world>1 branches: two torchrun ranks
+    share the GPU through the gloo backend; the all-reduced counts must equal
+    the oracle's for the doubled (weak-scaling) workload."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    sys.path.insert(0, ROOT)
+    import bench
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--workload", "cfg1", "--steps", "2", "--warmup", "1", "--dist-backend", "gloo",
+                        "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["config"]["walks_total"] == 2 << 20
+    off, adj = oracle.gen_erdos_renyi(65536, 524288, bench.GRAPH_SEED)
+    kv = oracle.uniform_start_counts(len(off) - 1, 2 << 20, bench.MASTER_SEED)
+    want = oracle.campaign_counts(off, adj, length=64, master=bench.MASTER_SEED, k_per_vertex=kv)
+    assert line["checksum"]["counts_sha256_16"] == bench.counts_checksum(want)

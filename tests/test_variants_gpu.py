@@ -42,7 +42,10 @@ CAMPAIGN_BIG = ["", "hot=0", "hot=1,hthreads=256", "hot=0,wpt=2", "c32=1", "fat=
 AESC_ENV = [{}, {"SABA_AESC_FAT": "0"}, {"SABA_AESC_FAT16": "0"}, {"SABA_AESC_BITMAP": "0"},
             {"SABA_AESC_BITMAP": "1"}, {"SABA_AESC_WORKERS": "1"}, {"SABA_AESC_WORKERS": "2"},
             {"SABA_AESC_PRIO": "0"}, {"SABA_PULL_STATIC": "1"}, {"SABA_DEPTHS_PER_GRAPH": "2"},
-            {"SABA_SHORT_STEPS": "0"}, {"SABA_SHORT_STEPS": "1000"}]
+            {"SABA_SHORT_STEPS": "0"}, {"SABA_SHORT_STEPS": "1000"},
+            {"SABA_AESC_REC": "2"}, {"SABA_AESC_REC": "2", "SABA_SHORT_STEPS": "0"},
+            {"SABA_AESC_FAT": "0", "SABA_AESC_FAT16": "0", "SABA_AESC_REC": "0"},
+            {"SABA_AESC_FAT": "0", "SABA_AESC_FAT16": "0", "SABA_AESC_REC": "0", "SABA_AESC_BITMAP": "1"}]
 
 
 def run_variant(spec, env_extra, tmp_path, tag):

@@ -52,3 +52,8 @@ if a.oracle_check:
     rel = np.abs(sub.g_hat - ref.g_hat) / (np.abs(ref.g_hat) + 1e-300)
     print(f"oracle check {len(chk)} sources ({time.time()-t:.1f}s): tau~ equal {ok_tt} "
           f"max rel {rel.max():.3e} pairs {sub.total_walk_pairs}=={ref.total_walk_pairs}", flush=True)
+import json  # noqa: E402
+print("AESC_JSON " + json.dumps({"workload": a.workload, "sources": int(a.sources), "walk_steps": est.total_walk_steps,
+                                 "walk_pairs": est.total_walk_pairs, "edge_visits": est.edge_visits,
+                                 "propagation_ms": est.propagation_ms, "walk_ms": est.walk_ms, "wall_s": wall}),
+      flush=True)
