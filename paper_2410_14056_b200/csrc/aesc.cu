@@ -273,12 +273,14 @@ __device__ __forceinline__ void rho_body(const double* __restrict__ P, const uin
 // list[count++] = x for every lane with `take`, one atomic per warp (all 32
 // lanes must call).
 __device__ __forceinline__ void warp_append(uint32_t* __restrict__ list, uint32_t* __restrict__ count,
-                                            uint32_t x, bool take, uint32_t lane) {
+                                            uint32_t x, bool take, uint32_t lane, uint32_t cap) {
     const uint32_t m = __ballot_sync(0xffffffffu, take);
     if (!m) return;
     uint32_t base = 0;
     if (lane == uint32_t(__ffs(m) - 1)) base = atomicAdd(count, uint32_t(__popc(m)));
     base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    SABA_DCHECK(base + uint32_t(__popc(m)) <= cap);  // every row is appended at most once per list
+    (void)cap;
     if (take) list[base + __popc(m & ((1u << lane) - 1u))] = x;
 }
 
@@ -291,7 +293,7 @@ __device__ __forceinline__ void expand_body(const uint2* __restrict__ csr, const
                                             uint32_t* __restrict__ ulist_next, uint32_t* __restrict__ ucount_next,
                                             uint32_t* __restrict__ flag, uint32_t* __restrict__ tflag,
                                             uint32_t* __restrict__ tlist, uint32_t* __restrict__ tcount,
-                                            const unsigned long long* __restrict__ ctrl) {
+                                            const unsigned long long* __restrict__ ctrl, uint32_t n) {
     const unsigned long long active = ctrl[kActive];
     if (!active || ctrl[kDense]) return;
     const uint32_t lane = threadIdx.x & 31;
@@ -311,13 +313,13 @@ __device__ __forceinline__ void expand_body(const uint2* __restrict__ csr, const
             }
             // appends are warp-aggregated: one counter atomic per warp, not
             // per row (a single global counter serialises in L2)
-            warp_append(ulist_next, ucount_next, x, claim, lane);
+            warp_append(ulist_next, ucount_next, x, claim, lane, n);
             bool fresh = false;
             if (claim && !tflag[x]) {  // x is claimed by exactly one thread per depth
                 tflag[x] = 1;
                 fresh = true;
             }
-            warp_append(tlist, tcount, x, fresh, lane);
+            warp_append(tlist, tcount, x, fresh, lane, n);
         }
     }
 }
@@ -334,7 +336,7 @@ __global__ void aesc_rho_expand(const double* __restrict__ P, const uint2* __res
                                 const unsigned long long* __restrict__ ctrl, uint32_t n, double* __restrict__ R,
                                 uint32_t* __restrict__ bits, uint32_t words) {
     rho_body(P, csr, ulist, ucount, ctrl, n, R, bits, words);
-    expand_body(csr, adj, M, ulist, ucount, ulist_next, ucount_next, flag, tflag, tlist, tcount, ctrl);
+    expand_body(csr, adj, M, ulist, ucount, ulist_next, ucount_next, flag, tflag, tlist, tcount, ctrl, n);
 }
 
 // Rows with more than kHeavy neighbours are split into fixed pieces of
@@ -463,6 +465,7 @@ __global__ void __launch_bounds__(256, SABA_PULL_MINB)
             if (lane == 0) nxt = uint32_t(atomicAdd(ctrl + kRowNext, 1ull));
             double a0 = 0.0, a1 = 0.0;
             unsigned long long mask = 0;
+            SABA_DCHECK(i < total);
             if (i < npieces) {
                 const HeavyPiece pc = pieces[i];
                 pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, need, a0, a1, mask);
@@ -592,6 +595,7 @@ __global__ void __launch_bounds__(128)
         for (uint32_t s = r.x + threadIdx.x; s < r.x + r.y; s += blockDim.x) {
             if (depth > tau_slot[s]) continue;
             const uint32_t j = adj[s];
+            SABA_DCHECK(j < p.n);
             g_hat[s] += pi - Pn[size_t(j) * kCols + c] * (1.0 / double(csr[j].y));
         }
     }
@@ -761,7 +765,9 @@ __global__ void __launch_bounds__(512)
     for (uint32_t i = threadIdx.x; i < T.count; i += blockDim.x) {
         const uint32_t w = S.start + T.t0 + i;
         const uint32_t d = top_bits(seed_of(G, w), 0, S.d1);
-        tmp[base[d] + atomicAdd(hist + d, 1u)] = w;
+        const uint32_t at = base[d] + atomicAdd(hist + d, 1u);
+        SABA_DCHECK(at >= S.start && at < S.start + S.size);  // coarse buckets stay inside their segment
+        tmp[at] = w;
     }
 }
 
@@ -820,6 +826,7 @@ __global__ void __launch_bounds__(256)
     for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
         const uint32_t w = S.d1 ? tmp[at + i] : S.start + i;
         const uint32_t r = atomicAdd(hist + top_bits(seed_of(G, w), S.d1, fb), 1u);
+        SABA_DCHECK(r < count && w >= G.walk_off && w < G.walk_off + 2 * G.pairs);
         if (staged)
             stage[r] = w;
         else
@@ -924,6 +931,7 @@ __global__ void __launch_bounds__(256, MINB)
                     } else {
                         cur[r] = adj_at<PACKED>(adj, adjp, rec[r].x + scaled_index(raw, rec[r].y));
                     }
+                    SABA_DCHECK(cur[r] < n);
                     if constexpr (BITMAP)
                         bw[r] = __ldg(bits + (bcol[r] + (cur[r] >> 5)));
                     else
@@ -1008,6 +1016,7 @@ __global__ void __launch_bounds__(256, MINB)
                     if (l >= 2) sc[r] += __hiloint2double(int(q[r].w), int(q[r].z));  // rho(x_{l-1})
                     const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
                     cur[r] = adj_at<PACKED>(adj, adjp, q[r].x + scaled_index(raw, q[r].y));
+                    SABA_DCHECK(cur[r] < n && q[r].y > 0);
                 }
         }
 #pragma unroll

@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(THREADS)
                 const uint32_t slot = rec[r].y >> shift;
                 if (l >= 2) {  // count the departing vertex x_{l-1}
                     const bool hot = act[r] && slot != 0;
+                    SABA_DCHECK(!hot || slot - 1 < nhot);
                     if (hot) atomicAdd(hot_cnt + (slot - 1), 1u);
                     if constexpr (AGG)
                         warp_count_visit(counts, cur[r], act[r] && !hot, lane);

@@ -34,6 +34,7 @@
 #include "device_graph.cuh"
 #include "hgraph.hpp"
 #include "saba_hash.cuh"
+#include "walk_common.cuh"
 
 namespace saba_cu {
 namespace {
@@ -120,6 +121,7 @@ __global__ void gb_hook(const uint64_t* __restrict__ keys, uint64_t two_m, uint3
             const uint32_t hi = max(ru, rv), lo = min(ru, rv);
             const uint32_t old = atomicCAS(parent + hi, hi, lo);
             if (old == hi) break;
+            SABA_DCHECK(old < hi);  // parents only ever point to smaller ids: no cycles
             ru = find_root(parent, old);
             rv = lo;
         }

@@ -4,6 +4,26 @@
 
 #include <cstdint>
 
+// Checked builds (tools/build_variant.sh checked "-DSABA_CHECKED"): device
+// asserts on the indices the cross-block protocols produce (frontier appends,
+// work-list hand-out, bucket scatters, hub-counter slots, walk vertices). The
+// compute-sanitizer is not available on the GPU pool, so these plus small
+// cases compared with the CPU reference stand in for memcheck.
+#ifdef SABA_CHECKED
+#include <cstdio>
+#define SABA_DCHECK(c)                                                                   \
+    do {                                                                                 \
+        if (!(c)) {                                                                      \
+            printf("SABA_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);           \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define SABA_DCHECK(c) \
+    do {               \
+    } while (0)
+#endif
+
 namespace saba_cu {
 
 // One 8-byte read-only gather of {base, degree} (LDG.E.64.CONSTANT).
