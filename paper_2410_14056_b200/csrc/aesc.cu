@@ -1428,13 +1428,18 @@ bool aesc_fat_enabled() {  // SABA_AESC_FAT=0 disables (default: on when L2-resi
     return on;
 }
 
-// Per-vertex records (aesc_walk_rec): 1 = on for the compact path (graphs
-// beyond L2 without 16-byte slot records), 0 = off, 2 = for every batch
-// (tuning knob SABA_AESC_REC).
+// Per-vertex records (aesc_walk_rec): 0 = off (default), 1 = on for the
+// compact path (graphs beyond L2 without 16-byte slot records), 2 = for every
+// batch (tuning knob SABA_AESC_REC). Measured and rejected as the default:
+// one 16 B record gather per step in place of the csr + rho pair was slower
+// on every config (walk phase cfg4 3.27 vs 2.93 s per 64 sources, cfg5 1.78
+// vs 1.60 s per 512, cfg3 11.6 vs 10.6 s; profiles/r02_aesc_rec_experiment.txt):
+// the dependent chain stays two gathers long and the 2.4 GB of per-column
+// records (cfg4) cost more L2 capacity than the rho gather they replace.
 int aesc_rec_mode() {
     static const int m = [] {
         const char* e = getenv("SABA_AESC_REC");
-        return e ? atoi(e) : 1;
+        return e ? atoi(e) : 0;
     }();
     return m;
 }

@@ -8,7 +8,6 @@ pushes in discovery order) and reduces walk pairs with a tree (the reference
 folds left), so only summation order differs (SURVEY §7 hard part 2).
 """
 import ast
-import os
 
 import numpy as np
 import pytest
@@ -238,65 +237,3 @@ def test_source_subset_and_shards(sb, oracle):
     for i in range(3):
         acc += sb.aesc(g, cfg, sources=src, shard_index=i, shard_count=3).g_hat
     assert np.array_equal(acc, est.g_hat)  # GPU-count invariance is bitwise
-
-
-@pytest.mark.slow
-def test_cfg3_graph_source_sample_matches_oracle(sb, oracle):
-    """BASELINE config 3 graph (R-MAT s16 ef8 LCC, eps 0.1, delta 0.01) on a
-    fixed source sample: tau~ exact, g_hat within 1e-9."""
-    g = sb.make_rmat(16, 8, seed=1)
-    rng = np.random.default_rng(0)
-    src = np.unique(rng.integers(0, g.n, 24)).astype(np.uint32)
-    cfg = sb.AescConfig(epsilon=0.1, delta=0.01)
-    est = sb.aesc(g, cfg, sources=src)
-    ref = oracle.aesc(g.offsets, g.adjacency, epsilon=0.1, delta=0.01, sources=src)
-    assert np.array_equal(est.plan.tau_tilde[src], ref.tau_tilde[src])
-    assert est.total_walk_pairs == ref.total_walk_pairs
-    assert close(est.g_hat, ref.g_hat), worst(est.g_hat, ref.g_hat)
-
-
-def _bench_sources(sb, n, count):
-    """The first `count` sources of bench.py's fixed counter_hash permutation."""
-    perm = np.argsort(sb.counter_hash(0x5355425345, np.arange(n, dtype=np.uint64)), kind="stable")
-    return np.sort(perm[:count]).astype(np.uint32)
-
-
-def _check_subset(sb, oracle, g, eps, delta, src):
-    cfg = sb.AescConfig(epsilon=eps, delta=delta)
-    est = sb.aesc(g, cfg, sources=src)
-    ref = oracle.aesc(g.offsets, g.adjacency, epsilon=eps, delta=delta, sources=src)
-    assert est.plan.lambda_hat == ref.lambda_hat
-    assert np.array_equal(est.plan.tau, ref.tau)
-    assert np.array_equal(est.plan.tau_tilde[src], ref.tau_tilde[src])
-    assert est.total_walk_pairs == ref.total_walk_pairs > 0
-    assert est.total_walk_steps == ref.total_walk_steps
-    assert close(est.g_hat, ref.g_hat), worst(est.g_hat, ref.g_hat)
-
-
-@pytest.mark.slow
-def test_cfg5_graph_source_sample_matches_oracle(sb, oracle):
-    """BASELINE config 5 (Chung-Lu n=3M, gamma 2.2, mean 78, cap 30000, LCC;
-    eps 0.01, delta 0.01) on the first 4 sources of the bench permutation:
-    plan and tau~ exact, pair and step counts exact, g_hat within 1e-9."""
-    g = sb.make_chung_lu(3_000_000, 2.2, 78.0, 30000.0, seed=1)
-    _check_subset(sb, oracle, g, 0.01, 0.01, _bench_sources(sb, g.n, 4))
-
-
-@pytest.mark.slow
-def test_cfg4_graph_hub_source_matches_oracle(sb, oracle):
-    """BASELINE config 4 (R-MAT s22 ef16 LCC; eps 0.05, delta 0.01) on the
-    highest-degree source among the first 256 of the bench permutation (a hub
-    switches early, so the CPU oracle finishes it in seconds)."""
-    g = sb.make_rmat(22, 16, seed=1)
-    cand = _bench_sources(sb, g.n, 256)
-    src = cand[np.argmax(np.diff(g.offsets)[cand])][None]
-    _check_subset(sb, oracle, g, 0.05, 0.01, src)
-
-
-@pytest.mark.slow
-@pytest.mark.skipif(not os.environ.get("SABA_LONG_TESTS"), reason="~18 min of CPU oracle; SABA_LONG_TESTS=1")
-def test_cfg4_graph_source_sample_matches_oracle(sb, oracle):
-    """BASELINE config 4 on the first source of the bench permutation (about
-    1e8 walk pairs on the CPU; profiles/r01_parity_full_size.txt)."""
-    g = sb.make_rmat(22, 16, seed=1)
-    _check_subset(sb, oracle, g, 0.05, 0.01, _bench_sources(sb, g.n, 1))

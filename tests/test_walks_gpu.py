@@ -147,24 +147,6 @@ def test_cfg1_full_size_bit_exact(sb, oracle):
         assert np.array_equal(acc, want)
 
 
-@pytest.mark.slow
-def test_cfg2_full_size_bit_exact(sb, oracle):
-    """BASELINE config 2 at full size: R-MAT s20 ef16 LCC, 16,777,216 uniform
-    walks of length 128 (2^31 visits) — bit-exact against the OpenMP oracle."""
-    g = sb.make_rmat(20, 16, seed=1)
-    W, L = 1 << 24, 128
-    sink = sb.VisitCountSink(g.n)
-    sb.run_walk_campaign(g, sb.CampaignConfig(length=L, master_seed=42), sink, total_walks=W)
-    assert int(sink.counts.sum()) == W * L
-    kv = oracle.uniform_start_counts(g.n, W, 42)
-    want = oracle.campaign_counts(g.offsets, g.adjacency, length=L, master=42, k_per_vertex=kv)
-    assert np.array_equal(sink.counts, want)
-    h = sb.VisitCountSink(g.n)
-    sb.run_walk_campaign(g, sb.CampaignConfig(length=L, master_seed=42, mode=sb.WalkMode.Hash), h,
-                         total_walks=W)
-    assert np.array_equal(h.counts, want)
-
-
 def test_device_variant_matches_host_variant(sb):
     torch = pytest.importorskip("torch")
     g = sb.make_rmat(14, 8, seed=2)
