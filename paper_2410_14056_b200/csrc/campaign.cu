@@ -85,6 +85,59 @@ __global__ void gen_keys_kernel(uint32_t n, const uint32_t* __restrict__ kv, uin
     }
 }
 
+// K1 fused (SABA mode): the same keys as gen_keys_kernel, sorted by seed
+// within each start vertex's share of the range by the warp that generates
+// them — a bitonic network over <= kSortCap seeds in the warp's slice of
+// shared memory — so no separate segmented sort pass (and no second key
+// buffer) is needed. A vertex holding more than kSortCap walks of the range
+// is sorted in runs of kSortCap (walk order is a performance device only:
+// counts are order-independent sums); the host picks this kernel when the
+// expected K_v is far below the cap.
+constexpr uint32_t kSortCap = 256;
+__global__ void __launch_bounds__(256)
+    gen_sorted_keys_kernel(uint32_t n, const uint32_t* __restrict__ kv, uint64_t k_uniform,
+                           const uint64_t* __restrict__ off, uint64_t r0, uint64_t r1, uint64_t master,
+                           uint64_t* __restrict__ keys, unsigned long long* __restrict__ counts) {
+    __shared__ uint32_t buf[8][kSortCap];
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t* sb = buf[threadIdx.x >> 5];
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t v = warp; v < n; v += nwarps) {
+        const uint64_t K = kv ? kv[v] : k_uniform;
+        const uint64_t o = kv ? off[v] : uint64_t(v) * k_uniform;
+        const uint64_t lo = o > r0 ? o : r0;
+        const uint64_t hi = (o + K) < r1 ? (o + K) : r1;
+        if (hi <= lo) continue;
+        if (lane == 0) counts[v] += hi - lo;  // step-0 visits; this warp owns v
+        const uint64_t vseed = substream(master, v);
+        for (uint64_t c0 = lo; c0 < hi; c0 += kSortCap) {
+            const uint32_t m = uint32_t(min(uint64_t(kSortCap), hi - c0));
+            uint32_t P = 32;
+            while (P < m) P <<= 1;
+            for (uint32_t i = lane; i < P; i += 32)
+                sb[i] = i < m ? walk_seed(vseed, c0 - o + i) : 0xffffffffu;  // padding sorts last
+            __syncwarp();
+            for (uint32_t size = 2; size <= P; size <<= 1)
+                for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (uint32_t i = lane; i < P; i += 32) {
+                        const uint32_t j = i ^ stride;
+                        if (j > i) {
+                            const uint32_t a = sb[i], b = sb[j];
+                            if ((a > b) == ((i & size) == 0)) {
+                                sb[i] = b;
+                                sb[j] = a;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            for (uint32_t i = lane; i < m; i += 32) keys[c0 - r0 + i] = (uint64_t(v) << 32) | sb[i];
+            __syncwarp();
+        }
+    }
+}
+
 // CT = counter type: uint32 per-launch counters (half the L2 footprint of
 // uint64) whenever a launch cannot overflow them, flushed into the uint64
 // sink by add_counts_kernel. PACKED = 21-bit packed adjacency.
@@ -254,6 +307,7 @@ struct WalkVariant {
     int hot = -1;           // hub counters in shared memory: 1 on, 0 off, -1 auto
     int hot_threads = 1024; // block size of the hub-counter kernel (256, 512, 1024)
     int hot_count = 0;      // hub table entries (0 = as many as shared memory holds)
+    int sort = -1;          // K1 SABA sort: 1 fused warp sort, 0 CUB segmented sort, -1 auto
 };
 
 WalkVariant walk_variant() {
@@ -274,6 +328,7 @@ WalkVariant walk_variant() {
             w.hot = get("hot=", w.hot);
             w.hot_threads = get("hthreads=", w.hot_threads);
             w.hot_count = get("hcount=", w.hot_count);
+            w.sort = get("sort=", w.sort);
         }
         return w;
     }();
@@ -640,8 +695,15 @@ uint64_t enqueue_campaign(saba_cu_graph* g, const saba_cu_campaign_config& c,
         ++*launches;
     }
     const uint64_t chunk_cap = std::min<uint64_t>(kChunkWalks, r1 - r0 ? r1 - r0 : 1);
+    // SABA sort fused into key generation when the walks per start vertex are
+    // well below the warp sort's cap (uniform starts: K_v ~ Poisson(W/n));
+    // large per-vertex campaigns keep the full segmented sort.
+    // SABA_WALK_VARIANT sort=0 forces the CUB segmented sort, sort=1 the fused one.
+    const double mean_k = uniform_starts ? double(c.total_walks) / double(n ? n : 1) : double(c.walks_per_vertex);
+    const int sort_knob = walk_variant().sort;
+    const bool fused_sort = c.mode == SABA_MODE_SABA && (sort_knob == 1 || (sort_knob < 0 && mean_k <= 64.0));
     uint64_t* keys = static_cast<uint64_t*>(g->keys.ensure(sizeof(uint64_t) * chunk_cap, st));
-    uint64_t* keys_alt = c.mode == SABA_MODE_SABA
+    uint64_t* keys_alt = c.mode == SABA_MODE_SABA && !fused_sort
                              ? static_cast<uint64_t*>(g->keys_alt.ensure(sizeof(uint64_t) * chunk_cap, st))
                              : nullptr;
     int* seg = static_cast<int*>(g->seg.ensure(sizeof(int) * (size_t(n) + 1), st));
@@ -653,12 +715,19 @@ uint64_t enqueue_campaign(saba_cu_graph* g, const saba_cu_campaign_config& c,
         const uint64_t b = std::min(r1, a + chunk_cap);
         const uint64_t nw = b - a;
         const int gb = int(std::min<uint64_t>((uint64_t(n) * 32 + 255) / 256, uint64_t(g->sm_count) * 32));
-        gen_keys_kernel<<<gb, 256, 0, st>>>(n, kv, c.walks_per_vertex, off, a, b, c.master_seed, keys,
-                                            seg, counts);
-        SABA_CUDA_CHECK(cudaGetLastError());
-        ++*launches;
         const uint64_t* walk_keys = keys;
-        if (c.mode == SABA_MODE_SABA) {
+        if (fused_sort) {  // K1 generate + per-vertex seed sort in one pass
+            gen_sorted_keys_kernel<<<gb, 256, 0, st>>>(n, kv, c.walks_per_vertex, off, a, b, c.master_seed, keys,
+                                                       counts);
+            SABA_CUDA_CHECK(cudaGetLastError());
+            ++*launches;
+        } else {
+            gen_keys_kernel<<<gb, 256, 0, st>>>(n, kv, c.walks_per_vertex, off, a, b, c.master_seed, keys,
+                                                seg, counts);
+            SABA_CUDA_CHECK(cudaGetLastError());
+            ++*launches;
+        }
+        if (c.mode == SABA_MODE_SABA && !fused_sort) {
             size_t tmp = 0;
             SABA_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, keys, keys_alt, int(nw),
                                                                int(n), seg, seg + 1, st));

@@ -37,8 +37,9 @@ CAMPAIGN_MID = ["", "fat=1,wpt=2", "fat=1,wpt=8", "fat=1,agg=0",
                 "fat=0,hot=1,packed=1", "fat=0,hot=1,packed=0", "fat=0,hot=1,hthreads=256",
                 "fat=0,hot=1,hthreads=512", "fat=0,hot=1,agg=0",
                 "fat=0,hot=0,wpt=1", "fat=0,hot=0,wpt=2", "fat=0,hot=0,wpt=8",
-                "fat=0,hot=0,packed=0", "fat=0,hot=0,agg=0", "c32=1", "c32=1,packed=0"]
-CAMPAIGN_BIG = ["", "hot=0", "hot=1,hthreads=256", "hot=0,wpt=2", "c32=1", "fat=1"]
+                "fat=0,hot=0,packed=0", "fat=0,hot=0,agg=0", "c32=1", "c32=1,packed=0",
+                "sort=0", "sort=1", "fat=0,hot=1,sort=0"]
+CAMPAIGN_BIG = ["", "hot=0", "hot=1,hthreads=256", "hot=0,wpt=2", "c32=1", "fat=1", "sort=0"]
 AESC_ENV = [{}, {"SABA_AESC_FAT": "0"}, {"SABA_AESC_FAT16": "0"}, {"SABA_AESC_BITMAP": "0"},
             {"SABA_AESC_BITMAP": "1"}, {"SABA_AESC_WORKERS": "1"}, {"SABA_AESC_WORKERS": "2"},
             {"SABA_AESC_PRIO": "0"}, {"SABA_PULL_STATIC": "1"}, {"SABA_DEPTHS_PER_GRAPH": "2"},
@@ -84,6 +85,22 @@ def test_campaign_variants_mid_graph(sb, oracle, tmp_path):
     spec = {"kind": "campaign", "graph": G_MID, "W": W, "L": L, "seed": seed, "hash": True, "shards": 2}
     got = run_variant(spec, {"SABA_WALK_VARIANT": "fat=0,hot=1"}, tmp_path, "mid_hash")["counts"]
     assert np.array_equal(got, want)
+
+
+def test_campaign_per_vertex_sort_paths(sb, oracle, tmp_path):
+    """K1's fused warp sort (K <= 256 per vertex), its run-wise form for larger
+    K, and the CUB segmented sort give the same counts (order is a performance
+    device only)."""
+    G = ["rmat", 10, 8, 2]
+    sys.path.insert(0, HERE)
+    from variant_worker import make_graph
+    g = make_graph(G)
+    for K in (37, 600):
+        want = oracle.campaign_counts(g.offsets, g.adjacency, K=K, length=11, master=8)
+        for v in ("", "sort=0", "sort=1"):
+            spec = {"kind": "campaign", "graph": G, "K": K, "L": 11, "seed": 8, "shards": 2 if v else 1}
+            got = run_variant(spec, {"SABA_WALK_VARIANT": v} if v else {}, tmp_path, f"pv{K}{v}")["counts"]
+            assert np.array_equal(got, want), (K, v)
 
 
 def test_campaign_variants_beyond_packed_ids(sb, oracle, tmp_path):

@@ -45,9 +45,11 @@ def main():
                                 mode=sb.WalkMode.Hash if spec.get("hash") else sb.WalkMode.Saba)
         parts = spec.get("shards", 1)
         acc = np.zeros(g.n, np.uint64)
+        if spec.get("K"):  # per-vertex campaign (walker.hpp:456-538)
+            cfg.walks_per_vertex = spec["K"]
         for i in range(parts):
             sink = sb.VisitCountSink(g.n)
-            sb.run_walk_campaign(g, cfg, sink, total_walks=spec["W"], shard_index=i, shard_count=parts)
+            sb.run_walk_campaign(g, cfg, sink, total_walks=spec.get("W", 0), shard_index=i, shard_count=parts)
             acc += sink.counts
         res["counts"] = acc
     else:
