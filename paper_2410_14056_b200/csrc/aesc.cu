@@ -903,6 +903,7 @@ __global__ void __launch_bounds__(256, MINB)
             for (int r = 0; r < WPT; ++r) rec[r] = len[r] > 1 ? ldg_csr(csr + cur[r]) : make_uint2(0, 1);
         }
         for (uint32_t l = 1; l < maxlen + 2; ++l) {
+            const StepHash shs = step_hash(mult, l);
             if constexpr (!FAT && !F16) {  // critical load of step l first
 #pragma unroll
                 for (int r = 0; r < WPT; ++r)
@@ -918,7 +919,7 @@ __global__ void __launch_bounds__(256, MINB)
 #pragma unroll
             for (int r = 0; r < WPT; ++r)
                 if (l < len[r]) {
-                    const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
+                    const uint32_t raw = seed[r] ^ hash_state_fast(shs, cur[r]);
                     if constexpr (F16) {
                         const uint4 f = __ldg(fat16 + (rec[r].x + scaled_index(raw, rec[r].y)));
                         cur[r] = f.x;
@@ -1006,6 +1007,7 @@ __global__ void __launch_bounds__(256, MINB)
         }
         maxlen = __reduce_max_sync(0xffffffffu, maxlen);
         for (uint32_t l = 1; l < maxlen; ++l) {
+            const StepHash shs = step_hash(mult, l);
             uint4 q[WPT];
 #pragma unroll
             for (int r = 0; r < WPT; ++r)
@@ -1014,7 +1016,7 @@ __global__ void __launch_bounds__(256, MINB)
             for (int r = 0; r < WPT; ++r)
                 if (l < len[r]) {
                     if (l >= 2) sc[r] += __hiloint2double(int(q[r].w), int(q[r].z));  // rho(x_{l-1})
-                    const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
+                    const uint32_t raw = seed[r] ^ hash_state_fast(shs, cur[r]);
                     cur[r] = adj_at<PACKED>(adj, adjp, q[r].x + scaled_index(raw, q[r].y));
                     SABA_DCHECK(cur[r] < n && q[r].y > 0);
                 }

@@ -161,13 +161,14 @@ __global__ void __launch_bounds__(kWalkThreads)
             seed[r] = uint32_t(k);
         }
         for (uint32_t l = 1; l < L; ++l) {
+            const StepHash shs = step_hash(mult, l);
             uint2 rec[WPT];
 #pragma unroll
             for (int r = 0; r < WPT; ++r) rec[r] = act[r] ? ldg_csr(csr + cur[r]) : make_uint2(0, 0);
             uint32_t nxt[WPT];
 #pragma unroll
             for (int r = 0; r < WPT; ++r) {
-                const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
+                const uint32_t raw = seed[r] ^ hash_state_fast(shs, cur[r]);
                 nxt[r] = act[r] ? adj_at<PACKED>(adj, adjp, rec[r].x + scaled_index(raw, rec[r].y)) : 0u;
             }
 #pragma unroll
@@ -209,9 +210,10 @@ __global__ void __launch_bounds__(kWalkThreads)
             deg[r] = rec.y;
         }
         for (uint32_t l = 1; l < L; ++l) {
+            const StepHash shs = step_hash(mult, l);
 #pragma unroll
             for (int r = 0; r < WPT; ++r) {
-                const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
+                const uint32_t raw = seed[r] ^ hash_state_fast(shs, cur[r]);
                 const uint64_t f = act[r] ? __ldg(reinterpret_cast<const unsigned long long*>(fat) +
                                                   sbase[r] + scaled_index(raw, deg[r]))
                                           : 0ull;
@@ -263,6 +265,7 @@ __global__ void __launch_bounds__(THREADS)
             seed[r] = uint32_t(k);
         }
         for (uint32_t l = 1; l < L; ++l) {
+            const StepHash shs = step_hash(mult, l);
             uint2 rec[WPT];
 #pragma unroll
             for (int r = 0; r < WPT; ++r) rec[r] = act[r] ? ldg_csr(csr_hot + cur[r]) : make_uint2(0, 0);
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(THREADS)
                     else
                         count_visit(counts, cur[r], act[r] && !hot);
                 }
-                const uint32_t raw = seed[r] ^ hash_state(mult, cur[r], l);
+                const uint32_t raw = seed[r] ^ hash_state_fast(shs, cur[r]);
                 cur[r] = act[r] ? adj_at<PACKED>(adj, adjp, rec[r].x + scaled_index(raw, deg)) : 0u;
             }
         }

@@ -38,6 +38,36 @@ SABA_HD uint32_t hash_state(uint64_t mult, uint32_t vertex, uint32_t step) {
     return static_cast<uint32_t>(x >> 32);
 }
 
+// hash_state split for the walk kernels, where every lane of a step shares
+// l. With M = mult = (m_hi, m_lo) and x = cur << 32 | l:
+//   x * M       = ((cur * m_lo) << 32) + l * M        (mod 2^64), so
+//   x1_hi       = cur * m_lo + hi32(l * M),  x1_lo = lo32(l * M)
+//   y = x1 ^ (x1 >> 47): only the low word changes: y_lo = x1_lo ^ (x1_hi >> 15)
+//   the final x ^= x >> 47 never reaches the returned high word, so
+//   h = hi32(y * M) = umulhi(y_lo, m_lo) + y_lo * m_hi + x1_hi * m_lo (mod 2^32).
+// Six 32-bit operations per lane instead of two full 64-bit products; equal
+// to hash_state bit for bit (tests/test_host.py checks the identity).
+struct StepHash {
+    uint32_t lm_lo, lm_hi, m_lo, m_hi;
+};
+SABA_HD StepHash step_hash(uint64_t mult, uint32_t step) {
+    const uint64_t lm = static_cast<uint64_t>(step) * mult;
+    return {static_cast<uint32_t>(lm), static_cast<uint32_t>(lm >> 32), static_cast<uint32_t>(mult),
+            static_cast<uint32_t>(mult >> 32)};
+}
+SABA_HD uint32_t mulhi32(uint32_t a, uint32_t b) {
+#if defined(__CUDA_ARCH__)
+    return __umulhi(a, b);
+#else
+    return static_cast<uint32_t>((static_cast<uint64_t>(a) * b) >> 32);
+#endif
+}
+SABA_HD uint32_t hash_state_fast(const StepHash& s, uint32_t vertex) {
+    const uint32_t x1_hi = vertex * s.m_lo + s.lm_hi;
+    const uint32_t y_lo = s.lm_lo ^ (x1_hi >> 15);
+    return mulhi32(y_lo, s.m_lo) + y_lo * s.m_hi + x1_hi * s.m_lo;
+}
+
 SABA_HD uint32_t scaled_index(uint32_t raw, uint32_t degree) {
 #if defined(__CUDA_ARCH__)
     return __umulhi(raw, degree);

@@ -149,3 +149,14 @@ def test_walk_budget_host(sb, golden):
         sb.walk_budget(0, 0.05, 0.05, 1, 10)
     with pytest.raises(ValueError):
         sb.walk_budget(1, 0.0, 0.05, 1, 10)
+
+
+def test_step_hash_identity(tmp_path):
+    """hash_state_fast (the walk kernels' per-step split of HashSpec::state,
+    rng.hpp:20-31) equals hash_state bit for bit over 2e7 random inputs."""
+    import subprocess
+    exe = str(tmp_path / "hash_identity")
+    subprocess.run(["g++", "-O2", "-I", os.path.join(ROOT, "paper_2410_14056_b200", "csrc"),
+                    os.path.join(ROOT, "tests", "cpp", "hash_identity.cpp"), "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0 and "mismatches 0" in r.stdout, r.stdout
