@@ -503,13 +503,16 @@ def run_ours(args):
 def aesc_roofline(name, est, wall_s):
     """Per-phase model (an honest AESC roofline):
     * propagation: the reference's edge-visits (sum over sources and depths of
-      the support degree sum, counted exactly on the device) x 12 B;
+      the support degree sum, counted exactly on the device) x 12 B, over the
+      propagation's CUDA-event time;
     * walks: DRAM bytes and L2 sectors per walk step measured by ncu on this
-      build for this config (profiles/aesc_walk_traffic.json), x steps.
-    Phase times are the per-batch CUDA-event spans summed over the batch
-    workers (two workers overlap, so each phase's rate is a lower bound)."""
+      build for this config (profiles/aesc_walk_traffic.json), x steps, over
+      the walk kernels' own CUDA-event time (events around every launch).
+    `est` should come from a one-worker run (AescConfig.workers=1): with two
+    batch workers the phases of different batches overlap and each phase's
+    event time includes the other's interference."""
     peak, peak_src = read_peak()
-    prop_s, walk_s = est.propagation_ms * 1e-3, est.walk_ms * 1e-3
+    prop_s, walk_s = est.propagation_ms * 1e-3, (est.walk_kernel_ms or est.walk_ms) * 1e-3
     prop_bytes = est.edge_visits * BYTES_PER_EDGE_VISIT
     prop_gbs = prop_bytes / prop_s / 1e9 if prop_s > 0 else 0.0
     tr = read_profile_json("aesc_walk_traffic.json", name) or {}
@@ -520,6 +523,7 @@ def aesc_roofline(name, est, wall_s):
         dram_gbs = tr["dram_bytes_per_step"] * est.total_walk_steps / walk_s / 1e9
         walk.update({"dram_bytes_per_step": tr["dram_bytes_per_step"], "achieved_dram_gbs": dram_gbs,
                      "dram_frac": dram_gbs / peak})
+    l2 = None
     if tr.get("l2_sector_bytes_per_step") is not None and walk_s > 0:
         l2 = tr["l2_sector_bytes_per_step"] * est.total_walk_steps / walk_s / 1e9
         walk.update({"l2_sector_bytes_per_step": tr["l2_sector_bytes_per_step"], "achieved_l2_gbs": l2,
@@ -533,7 +537,14 @@ def aesc_roofline(name, est, wall_s):
         roof = {"bound": "hbm", "achieved": dram_gbs, "peak": peak, "unit": "GB/s", "frac": dram_gbs / peak,
                 "traffic": tr.get("dram_bytes_per_launch"), "kernel": "aesc_walk_sorted (K4 walk phase)",
                 "model": "ncu-measured DRAM bytes per walk step (this build, this config) x walk steps / "
-                         "K4 phase time"}
+                         "K4 kernel time"}
+        if l2 is not None:
+            # L2-resident configs (cfg3): the walk is bound by L2 random-sector
+            # throughput, not HBM; the ceiling is measured (gather_ceiling.cu)
+            roof["l2"] = {"achieved_sector_gbs": l2, "ceiling_gbs": L2_RANDOM_SECTOR_GBS,
+                          "frac": l2 / L2_RANDOM_SECTOR_GBS,
+                          "ceiling_source": "tools/gather_ceiling.cu random 32 B-sector gathers, 32 MB working set "
+                                            "(profiles/r01_gather_ceiling.txt)"}
     else:
         roof = {"bound": "hbm", "achieved": prop_gbs, "peak": peak, "unit": "GB/s", "frac": prop_gbs / peak,
                 "traffic": None, "kernel": "aesc_pull (K3 propagation)",
@@ -571,6 +582,10 @@ def aesc_block(sb, args, name, dev_index):
     e1.synchronize()
     e2e = e0.elapsed_time(e1) * 1e-3
     assert np.array_equal(est2.s_hat, est.s_hat), "e2e AESC differs from the device run"
+    # roofline run: one batch worker, so each phase's CUDA-event time is its own
+    cfg1 = sb.AescConfig(epsilon=eps, delta=delta, threads=1, workers=1)
+    est1 = sb.aesc(g, cfg1, device=dev_index)
+    assert np.array_equal(est1.s_hat, est.s_hat), "the one-worker run differs"
     res = {"metric": "TGT+ all-edges SC wall time", "value": wall, "unit": "s", "higher_is_better": False,
            "steps": 1, "warmup": 1, "dtype": "f64",
            "config": aesc_config(name, g.n, g.m, 1, f"all {g.n} sources"),
@@ -579,7 +594,9 @@ def aesc_block(sb, args, name, dev_index):
                      "edge_visits": est.edge_visits, "lambda_hat": est.plan.lambda_hat,
                      "tau": int(est.plan.max_tau), "plan_s": est.plan_seconds,
                      "propagation_s": est.propagation_ms * 1e-3, "walk_s": est.walk_ms * 1e-3},
-           "roofline": aesc_roofline(name, est, wall),
+           "roofline": dict(aesc_roofline(name, est1, wall), roofline_run={
+               "workers": est1.workers, "seconds": est1.seconds, "propagation_s": est1.propagation_ms * 1e-3,
+               "walk_kernel_s": est1.walk_kernel_ms * 1e-3, "walk_phase_s": est1.walk_ms * 1e-3}),
            "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(g.offsets.nbytes + g.adjacency.nbytes),
                    "d2h_bytes_per_step": int(est.g_hat.nbytes + est.s_hat.nbytes)},
            "gpu_launches": int(est.launches), "clocks": clk.summary()}
@@ -680,6 +697,10 @@ def run_aesc_bench(args):
         e1.synchronize()
         e2e.append(e0.elapsed_time(e1) * 1e-3)
     assert np.array_equal(host.numpy(), gh), "e2e g_hat differs from the device run"
+    # roofline run of this rank's shard with one batch worker (phase times not overlapped)
+    est1 = sb.aesc_device(g, sb.AescConfig(epsilon=eps, delta=delta, threads=1, workers=1), g_hat.data_ptr(),
+                          stream.cuda_stream, sources=sources, shard_index=rank, shard_count=world,
+                          device=dev_index)
     e2e_t = torch.tensor([sum(e2e)], dtype=torch.float64, device=dev)
     edge_visits = torch.tensor([float(ests[-1].edge_visits)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -708,7 +729,10 @@ def run_aesc_bench(args):
             "stats": {"walk_pairs_rank0": est.total_walk_pairs, "walk_steps_rank0": est.total_walk_steps,
                       "edge_visits_rank0": est.edge_visits, "plan_s": est.plan_seconds,
                       "propagation_s_rank0": est.propagation_ms * 1e-3, "walk_s_rank0": est.walk_ms * 1e-3},
-            "roofline": aesc_roofline(args.workload, est, measured),
+            "roofline": dict(aesc_roofline(args.workload, est1, measured), roofline_run={
+                "workers": est1.workers, "seconds": est1.seconds, "propagation_s": est1.propagation_ms * 1e-3,
+                "walk_kernel_s": est1.walk_kernel_ms * 1e-3, "walk_phase_s": est1.walk_ms * 1e-3,
+                "rank": 0}),
             "cpu_baseline": cpu,
             # the e2e-only work (pinned CSR upload, device replica build) is a
             # per-run cost: added once, not multiplied by the extrapolation

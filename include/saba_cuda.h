@@ -223,7 +223,7 @@ typedef struct {
     uint32_t lanes;
     uint32_t max_truncation;
     int32_t per_edge_tau;
-    int32_t reserved;
+    int32_t workers;          /* extension: batch workers per device (0 = auto; results unchanged) */
     int64_t switch_depth_cap;
     uint64_t hash_multiplier;
 } saba_cu_aesc_config;
@@ -243,6 +243,8 @@ typedef struct {
     uint32_t max_tau;
     uint32_t launches;
     uint32_t replicas;         /* device replicas that ran shards of this call */
+    uint32_t workers;          /* batch workers per replica */
+    double walk_kernel_ms;     /* K4 walk kernels alone (events around each launch), summed */
 } saba_cu_aesc_report;
 
 /* walk_budget (aesc.hpp:117-126). */

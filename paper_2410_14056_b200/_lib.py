@@ -44,7 +44,7 @@ class AescConfigC(C.Structure):
                 ("power_iterations", C.c_uint32), ("candidate_nodes", C.c_uint32),
                 ("mode", C.c_int32), ("threads", C.c_int32), ("master_seed", C.c_uint64),
                 ("lanes", C.c_uint32), ("max_truncation", C.c_uint32),
-                ("per_edge_tau", C.c_int32), ("reserved", C.c_int32),
+                ("per_edge_tau", C.c_int32), ("workers", C.c_int32),
                 ("switch_depth_cap", C.c_int64), ("hash_multiplier", C.c_uint64)]
 
 
@@ -54,7 +54,8 @@ class AescReportC(C.Structure):
                 ("total_walk_pairs", C.c_uint64), ("total_walk_steps", C.c_uint64),
                 ("edge_visits", C.c_uint64), ("sources", C.c_uint64),
                 ("lambda_hat", C.c_double), ("bipartite", C.c_int32), ("clamped", C.c_int32),
-                ("max_tau", C.c_uint32), ("launches", C.c_uint32), ("replicas", C.c_uint32)]
+                ("max_tau", C.c_uint32), ("launches", C.c_uint32), ("replicas", C.c_uint32),
+                ("workers", C.c_uint32), ("walk_kernel_ms", C.c_double)]
 
 
 vp = C.c_void_p

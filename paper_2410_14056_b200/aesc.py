@@ -31,12 +31,13 @@ class AescConfig:
     per_edge_tau: bool = False
     switch_depth_cap: int = -1
     hash: HashSpec = field(default_factory=HashSpec)
+    workers: int = 0  # extension: batch workers per device (0 = auto); never changes results
 
     def to_c(self) -> L.AescConfigC:
         return L.AescConfigC(self.epsilon, self.delta, self.power_iterations, self.candidate_nodes,
                              int(self.mode), self.threads, self.master_seed, self.lanes,
-                             self.max_truncation, int(self.per_edge_tau), 0, self.switch_depth_cap,
-                             self.hash.multiplier)
+                             self.max_truncation, int(self.per_edge_tau), self.workers,
+                             self.switch_depth_cap, self.hash.multiplier)
 
 
 @dataclass
@@ -88,6 +89,8 @@ class CentralityEstimate:
     edge_visits: int = 0
     launches: int = 0
     replicas: int = 1
+    workers: int = 1
+    walk_kernel_ms: float = 0.0
 
 
 def walk_budget(tau_effective: int, epsilon: float, delta: float, degree: int,
@@ -152,7 +155,8 @@ def aesc(g: Graph, cfg: AescConfig, *, sources=None, shard_index: int = 0, shard
     plan = TruncationPlan(tau, tt, rep.lambda_hat, bool(rep.clamped), rep.max_tau)
     return CentralityEstimate(s_hat, g_hat, cfg, plan, bool(rep.bipartite), rep.total_walk_pairs,
                               rep.total_walk_steps, rep.seconds, rep.propagation_ms, rep.walk_ms,
-                              rep.plan_seconds, rep.edge_visits, rep.launches, rep.replicas)
+                              rep.plan_seconds, rep.edge_visits, rep.launches, rep.replicas, rep.workers,
+                              rep.walk_kernel_ms)
 
 
 def aesc_device(g: Graph, cfg: AescConfig, g_hat_dev_ptr: int, stream_ptr: int = 0, *, sources=None,
@@ -175,7 +179,8 @@ def aesc_device(g: Graph, cfg: AescConfig, g_hat_dev_ptr: int, stream_ptr: int =
     plan = TruncationPlan(tau, tt, rep.lambda_hat, bool(rep.clamped), rep.max_tau)
     return CentralityEstimate(None, None, cfg, plan, bool(rep.bipartite), rep.total_walk_pairs,
                               rep.total_walk_steps, rep.seconds, rep.propagation_ms, rep.walk_ms,
-                              rep.plan_seconds, rep.edge_visits, rep.launches, rep.replicas)
+                              rep.plan_seconds, rep.edge_visits, rep.launches, rep.replicas, rep.workers,
+                              rep.walk_kernel_ms)
 
 
 def symmetrise(g: Graph, g_hat_dev_ptr: int, s_hat_dev_ptr: int, stream_ptr: int = 0,

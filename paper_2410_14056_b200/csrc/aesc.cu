@@ -95,7 +95,10 @@ struct AescState {
     cudaStream_t stream_walk = nullptr;  // walk phase of the batch workers
     uint64_t* h_ctrl = nullptr;  // pinned mirror of the control block
     bool slot_edge_ready = false;  // slot_edge_d holds the slot -> edge map (K5)
+    cudaEvent_t ev_walk[2] = {nullptr, nullptr};  // around each walk-kernel launch (report)
     ~AescState() {
+        for (cudaEvent_t e : ev_walk)
+            if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
         if (stream_walk) cudaStreamDestroy(stream_walk);
         if (h_ctrl) cudaFreeHost(h_ctrl);
@@ -1125,6 +1128,7 @@ struct Engine {
             SABA_CUDA_CHECK(cudaStreamCreateWithPriority(&st->stream, cudaStreamNonBlocking, hi));
             SABA_CUDA_CHECK(cudaStreamCreateWithPriority(&st->stream_walk, cudaStreamNonBlocking, lo));
             SABA_CUDA_CHECK(cudaHostAlloc(&st->h_ctrl, sizeof(uint64_t) * kCtrlWords, cudaHostAllocDefault));
+            for (cudaEvent_t& e : st->ev_walk) SABA_CUDA_CHECK(cudaEventCreate(&e));
         }
         s = st->stream;
         const uint32_t n = g->n;
@@ -1572,7 +1576,7 @@ void walk_dispatch(const Launch& L, bool fat, bool packed, bool f16) {
 
 void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb, const double* R,
                const uint32_t* bits, uint64_t mult, double* g_hat_dev, uint32_t* launches,
-               const uint4* recs = nullptr) {
+               const uint4* recs = nullptr, float* walk_kernel_ms = nullptr) {
     const uint32_t words = (g->n + 31) / 32;
     if (tb.empty()) return;
     double* part = static_cast<double*>(st->partials.ensure(sizeof(double) * std::max(tb.ntiles, 1u)));
@@ -1601,16 +1605,23 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         }();
         const bool short_walks = c.steps < short_steps * nw;
         const Launch L{out_g, out_w, nw, dg, g, R, bits, words, mult, score, s, recs};
+        if (walk_kernel_ms) SABA_CUDA_CHECK(cudaEventRecord(st->ev_walk[0], s));
         if (short_walks)
             walk_dispatch<kShortWpt, kShortMinb>(L, fat, packed, f16);
         else
             walk_dispatch<4, 5>(L, fat, packed, false);
         SABA_CUDA_CHECK(cudaGetLastError());
+        if (walk_kernel_ms) SABA_CUDA_CHECK(cudaEventRecord(st->ev_walk[1], s));
         aesc_pair_reduce<<<int(std::min<uint32_t>(nt, g->sm_count * 8)), 256, 0, s>>>(dt, nt, dg, score, part);
         SABA_CUDA_CHECK(cudaGetLastError());
         *launches += 2;
         // the chunk's host metadata must outlive its uploads
         SABA_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (walk_kernel_ms) {
+            float ms = 0.f;
+            SABA_CUDA_CHECK(cudaEventElapsedTime(&ms, st->ev_walk[0], st->ev_walk[1]));
+            *walk_kernel_ms += ms;
+        }
     }
     const uint32_t nsw = uint32_t(tb.slots.size());
     auto* ds = static_cast<SlotWork*>(st->slots.ensure(sizeof(SlotWork) * nsw));
@@ -1760,6 +1771,8 @@ struct AescRun {
     std::vector<uint32_t> tt_all;   // tau~ per vertex (0 outside this call's sources)
     uint64_t pairs = 0, steps = 0, edge_visits = 0, nsources = 0;
     float prop_ms = 0.f, walk_ms = 0.f;
+    double walk_kernel_ms = 0.0;
+    int workers = 1;
     uint32_t launches = 0;
     double seconds = 0.0, plan_seconds = 0.0;
     cudaStream_t root_stream = nullptr;
@@ -1782,6 +1795,8 @@ void fill_aesc_report(const AescRun& run, saba_cu_aesc_report* rep) {
     r.max_tau = run.plan.max_tau;
     r.launches = run.launches;
     r.replicas = uint32_t(run.reps.size());
+    r.workers = uint32_t(run.workers);
+    r.walk_kernel_ms = run.walk_kernel_ms;
     *rep = r;
 }
 
@@ -1841,7 +1856,9 @@ void aesc_run(saba_cu_graph* g, const saba_cu_aesc_config& cfg, const uint32_t* 
     const size_t nbatches = (list.size() + kCols - 1) / kCols;
     // (measured: 3 workers gain nothing on cfg3/cfg4; 2 beat 1 on cfg3 and,
     // since the walk phase got cheaper, on the shallow cfg5 plan too: -11%)
-    const int nworkers = workers_env ? workers_env : (nbatches > R ? kWorkspaces : 1);
+    const int nworkers = cfg.workers > 0 ? std::min(cfg.workers, kWorkspaces)
+                         : workers_env ? workers_env : (nbatches > R ? kWorkspaces : 1);
+    out.workers = nworkers;
     std::vector<std::unique_ptr<Engine>> engines;  // replica-major: engines[r * nworkers + w]
     std::vector<std::unique_lock<std::recursive_mutex>> locks;
     out.d_g.assign(R, nullptr);
@@ -1872,7 +1889,7 @@ void aesc_run(saba_cu_graph* g, const saba_cu_aesc_config& cfg, const uint32_t* 
     lap("workers ready");
     out.tt_all.assign(n, 0);
     const size_t nthreads = engines.size();
-    std::vector<float> prop_ms(nthreads, 0.f), walk_ms(nthreads, 0.f);
+    std::vector<float> prop_ms(nthreads, 0.f), walk_ms(nthreads, 0.f), walk_kms(nthreads, 0.f);
     std::vector<std::exception_ptr> failure(nthreads);
     std::atomic<size_t> next_batch{0};
     const auto t0 = std::chrono::steady_clock::now();
@@ -1946,7 +1963,7 @@ void aesc_run(saba_cu_graph* g, const saba_cu_aesc_config& cfg, const uint32_t* 
                 }
                 run_tiles(rg, W.st, W.st->stream_walk, tb, W.st->R.as<double>(),
                           use_bits && !use_rec ? W.st->bits.as<uint32_t>() : nullptr, cfg.hash_multiplier, d_g,
-                          &W.launches, recs);
+                          &W.launches, recs, &walk_kms[wi]);
                 SABA_CUDA_CHECK(cudaEventRecord(e2, W.s));
                 const auto h3 = std::chrono::steady_clock::now();
                 W.clear_batch(int(cols.size()));
@@ -1990,6 +2007,7 @@ void aesc_run(saba_cu_graph* g, const saba_cu_aesc_config& cfg, const uint32_t* 
         out.edge_visits += E.read_ctrl(kEdgeVisits);
         out.prop_ms += prop_ms[w];
         out.walk_ms += walk_ms[w];
+        out.walk_kernel_ms += walk_kms[w];
     }
     // one combine of the replicas' g_hat (single writer per slot: exact)
     std::vector<void*> ptrs(out.d_g.begin(), out.d_g.end());

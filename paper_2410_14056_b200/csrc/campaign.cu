@@ -113,7 +113,18 @@ __global__ void __launch_bounds__(256)
         const uint64_t vseed = substream(master, v);
         for (uint64_t c0 = lo; c0 < hi; c0 += kSortCap) {
             const uint32_t m = uint32_t(min(uint64_t(kSortCap), hi - c0));
-            uint32_t P = 32;
+            if (m <= 32) {  // one seed per lane: the bitonic network over shuffles
+                uint32_t x = lane < m ? walk_seed(vseed, c0 - o + lane) : 0xffffffffu;
+                for (uint32_t size = 2; size <= 32; size <<= 1)
+                    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, stride);
+                        const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
+                        x = keep_min ? min(x, y) : max(x, y);
+                    }
+                if (lane < m) keys[c0 - r0 + lane] = (uint64_t(v) << 32) | x;
+                continue;
+            }
+            uint32_t P = 64;
             while (P < m) P <<= 1;
             for (uint32_t i = lane; i < P; i += 32)
                 sb[i] = i < m ? walk_seed(vseed, c0 - o + i) : 0xffffffffu;  // padding sorts last

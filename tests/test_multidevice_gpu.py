@@ -42,6 +42,10 @@ def test_aesc_device_lists_bit_identical(sb):
     cfg = sb.AescConfig(epsilon=0.15, delta=0.05)
     one = sb.aesc(g, cfg)
     assert one.replicas == 1
+    for w in (1, 2):  # batch workers per device (AescConfig.workers): same bits
+        ew = sb.aesc(g, sb.AescConfig(epsilon=0.15, delta=0.05, workers=w))
+        assert ew.workers == w and np.array_equal(ew.g_hat, one.g_hat) and np.array_equal(ew.s_hat, one.s_hat)
+        assert ew.walk_kernel_ms > 0
     for devs in ([0, 0], [0, 0, 0]):
         est = sb.aesc(g, cfg, devices=devs)
         assert est.replicas == len(devs)
