@@ -245,6 +245,8 @@ typedef struct {
     uint32_t replicas;         /* device replicas that ran shards of this call */
     uint32_t workers;          /* batch workers per replica */
     double walk_kernel_ms;     /* K4 walk kernels alone (events around each launch), summed */
+    double setup_seconds;      /* per-call setup between the plan and the first batch (slot records,
+                                  workspaces, tau upload): like the plan, not per-source work */
 } saba_cu_aesc_report;
 
 /* walk_budget (aesc.hpp:117-126). */

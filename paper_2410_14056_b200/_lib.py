@@ -55,7 +55,7 @@ class AescReportC(C.Structure):
                 ("edge_visits", C.c_uint64), ("sources", C.c_uint64),
                 ("lambda_hat", C.c_double), ("bipartite", C.c_int32), ("clamped", C.c_int32),
                 ("max_tau", C.c_uint32), ("launches", C.c_uint32), ("replicas", C.c_uint32),
-                ("workers", C.c_uint32), ("walk_kernel_ms", C.c_double)]
+                ("workers", C.c_uint32), ("walk_kernel_ms", C.c_double), ("setup_seconds", C.c_double)]
 
 
 vp = C.c_void_p

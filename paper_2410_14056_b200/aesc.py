@@ -91,6 +91,7 @@ class CentralityEstimate:
     replicas: int = 1
     workers: int = 1
     walk_kernel_ms: float = 0.0
+    setup_seconds: float = 0.0
 
 
 def walk_budget(tau_effective: int, epsilon: float, delta: float, degree: int,
@@ -156,7 +157,7 @@ def aesc(g: Graph, cfg: AescConfig, *, sources=None, shard_index: int = 0, shard
     return CentralityEstimate(s_hat, g_hat, cfg, plan, bool(rep.bipartite), rep.total_walk_pairs,
                               rep.total_walk_steps, rep.seconds, rep.propagation_ms, rep.walk_ms,
                               rep.plan_seconds, rep.edge_visits, rep.launches, rep.replicas, rep.workers,
-                              rep.walk_kernel_ms)
+                              rep.walk_kernel_ms, rep.setup_seconds)
 
 
 def aesc_device(g: Graph, cfg: AescConfig, g_hat_dev_ptr: int, stream_ptr: int = 0, *, sources=None,
@@ -180,7 +181,7 @@ def aesc_device(g: Graph, cfg: AescConfig, g_hat_dev_ptr: int, stream_ptr: int =
     return CentralityEstimate(None, None, cfg, plan, bool(rep.bipartite), rep.total_walk_pairs,
                               rep.total_walk_steps, rep.seconds, rep.propagation_ms, rep.walk_ms,
                               rep.plan_seconds, rep.edge_visits, rep.launches, rep.replicas, rep.workers,
-                              rep.walk_kernel_ms)
+                              rep.walk_kernel_ms, rep.setup_seconds)
 
 
 def symmetrise(g: Graph, g_hat_dev_ptr: int, s_hat_dev_ptr: int, stream_ptr: int = 0,

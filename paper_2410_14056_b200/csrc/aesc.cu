@@ -1772,6 +1772,7 @@ struct AescRun {
     uint64_t pairs = 0, steps = 0, edge_visits = 0, nsources = 0;
     float prop_ms = 0.f, walk_ms = 0.f;
     double walk_kernel_ms = 0.0;
+    double setup_seconds = 0.0;  // plan end -> first batch (per-call, not per-source, work)
     int workers = 1;
     uint32_t launches = 0;
     double seconds = 0.0, plan_seconds = 0.0;
@@ -1797,6 +1798,7 @@ void fill_aesc_report(const AescRun& run, saba_cu_aesc_report* rep) {
     r.replicas = uint32_t(run.reps.size());
     r.workers = uint32_t(run.workers);
     r.walk_kernel_ms = run.walk_kernel_ms;
+    r.setup_seconds = run.setup_seconds;
     *rep = r;
 }
 
@@ -1893,6 +1895,7 @@ void aesc_run(saba_cu_graph* g, const saba_cu_aesc_config& cfg, const uint32_t* 
     std::vector<std::exception_ptr> failure(nthreads);
     std::atomic<size_t> next_batch{0};
     const auto t0 = std::chrono::steady_clock::now();
+    out.setup_seconds = std::chrono::duration<double>(t0 - t_plan1).count();
     auto worker = [&](size_t wi) {
         try {
             Engine& W = *engines[wi];

@@ -310,6 +310,75 @@ __global__ void __launch_bounds__(THREADS)
         if (hot_cnt[i]) atomicAdd(counts + hot_vertex[i], (unsigned long long)hot_cnt[i]);
 }
 
+// K2 over degree-ranked records (see saba_cu_graph::d_rec). A walk carries
+// the RANK r of its vertex: one 8-byte gather rec[r] yields the vertex id (for
+// the hash and the count), its base and its degree; the neighbour slot holds
+// the neighbour's rank. Records are laid out by descending degree, so the
+// records of the most visited vertices (a walk is at v with probability
+// ~ deg(v) / 2m) share a few KB of lines that stay in L1, and hubs are simply
+// r < nhot (their counters live in shared memory). Walks, selections and the
+// counted multiset are exactly those of walk_count_hot_kernel.
+template <int WPT, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+    walk_count_rec_kernel(const uint64_t* __restrict__ rec, const uint32_t* __restrict__ rank,
+                          const uint64_t* __restrict__ adj_rank, uint32_t nb, uint32_t db, uint32_t nhot,
+                          const uint64_t* __restrict__ keys, uint64_t nwalks, uint32_t L, uint64_t mult,
+                          unsigned long long* __restrict__ counts) {
+    extern __shared__ uint32_t hot_cnt[];
+    for (uint32_t i = threadIdx.x; i < nhot; i += blockDim.x) hot_cnt[i] = 0;
+    __syncthreads();
+    const uint64_t idmask = (uint64_t(1) << nb) - 1, bmask = (uint64_t(1) << (db - nb)) - 1;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t base = warp * 32 * WPT; base < nwalks; base += nwarps * 32 * WPT) {
+        uint32_t cur[WPT], seed[WPT];  // cur = rank of the walk's vertex
+        bool act[WPT];
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {
+            const uint64_t i = base + uint64_t(r) * 32 + lane;
+            act[r] = i < nwalks;
+            const uint64_t k = act[r] ? __ldcs(reinterpret_cast<const unsigned long long*>(keys) + i) : 0;
+            cur[r] = act[r] ? __ldg(rank + uint32_t(k >> 32)) : 0u;
+            seed[r] = uint32_t(k);
+        }
+        for (uint32_t l = 1; l < L; ++l) {
+            const StepHash shs = step_hash(mult, l);
+            uint64_t q[WPT];
+#pragma unroll
+            for (int r = 0; r < WPT; ++r)
+                q[r] = act[r] ? __ldg(reinterpret_cast<const unsigned long long*>(rec) + cur[r]) : 0ull;
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) {
+                const uint32_t id = uint32_t(q[r] & idmask);
+                const uint32_t sbase = uint32_t((q[r] >> nb) & bmask);
+                const uint32_t deg = uint32_t(q[r] >> db);
+                if (l >= 2) {  // count the departing vertex x_{l-1}
+                    const bool hot = act[r] && cur[r] < nhot;
+                    if (hot) atomicAdd(hot_cnt + cur[r], 1u);
+                    warp_count_visit(counts, id, act[r] && !hot, lane);
+                }
+                const uint32_t raw = seed[r] ^ hash_state_fast(shs, id);
+                cur[r] = act[r] ? adj_at<true>(nullptr, adj_rank, sbase + scaled_index(raw, deg)) : 0u;
+                SABA_DCHECK(!act[r] || deg > 0);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {  // the last vertex x_{L-1}
+            const bool last = act[r] && L > 1;
+            const bool hot = last && cur[r] < nhot;
+            if (hot) atomicAdd(hot_cnt + cur[r], 1u);
+            const uint32_t id = last && !hot
+                                    ? uint32_t(__ldg(reinterpret_cast<const unsigned long long*>(rec) + cur[r]) & idmask)
+                                    : 0u;
+            warp_count_visit(counts, id, last && !hot, lane);
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nhot; i += blockDim.x)
+        if (hot_cnt[i]) atomicAdd(counts + uint32_t(rec[i] & idmask), (unsigned long long)hot_cnt[i]);
+}
+
 // Kernel variant (tuning knob; SABA_WALK_VARIANT="wpt=4,packed=1,c32=1,agg=1").
 struct WalkVariant {
     int wpt = 4;
@@ -322,6 +391,7 @@ struct WalkVariant {
     int hot_threads = 1024; // block size of the hub-counter kernel (256, 512, 1024)
     int hot_count = 0;      // hub table entries (0 = as many as shared memory holds)
     int sort = -1;          // K1 SABA sort: 1 fused warp sort, 0 CUB segmented sort, -1 auto
+    int rec = -1;           // degree-ranked records (walk_count_rec_kernel): 1 on, 0 off, -1 auto
 };
 
 WalkVariant walk_variant() {
@@ -343,6 +413,7 @@ WalkVariant walk_variant() {
             w.hot_threads = get("hthreads=", w.hot_threads);
             w.hot_count = get("hcount=", w.hot_count);
             w.sort = get("sort=", w.sort);
+            w.rec = get("rec=", w.rec);
         }
         return w;
     }();
@@ -412,6 +483,90 @@ bool ensure_hot(saba_cu_graph* g) {
     return true;
 }
 
+
+__global__ void rec_build_kernel(const uint32_t* __restrict__ sorted_id, const uint2* __restrict__ csr, uint32_t n,
+                                 uint32_t nb, uint32_t db, uint64_t* __restrict__ rec, uint32_t* __restrict__ rank) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t v = sorted_id[i];
+        const uint2 r = csr[v];
+        rec[i] = uint64_t(v) | (uint64_t(r.x) << nb) | (uint64_t(r.y) << db);
+        rank[v] = i;
+    }
+}
+
+__global__ void rank_adj_kernel(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ rank, uint64_t two_m,
+                                uint64_t* __restrict__ packed) {
+    const uint64_t words = (two_m + 2) / 3;
+    for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < words;
+         w += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t x = 0;
+        for (uint32_t q = 0; q < 3; ++q) {
+            const uint64_t s = 3 * w + q;
+            if (s < two_m) x |= uint64_t(rank[adj[s]]) << (kPackBits * q);
+        }
+        packed[w] = x;
+    }
+}
+
+// Degree-ranked records (walk_count_rec_kernel), built on the device once per
+// graph: the same stable descending-degree order as the hub table, so the hub
+// test r < hot_count picks exactly the hot kernel's hubs. Needs ranks that pack
+// into 21 bits and {id, base, degree} in 64 bits.
+bool ensure_rec(saba_cu_graph* g) {
+    if (g->rec_tried) return g->d_rec != nullptr;
+    g->rec_tried = true;
+    if (g->n == 0 || g->n > kPackMax || !ensure_hot(g)) return false;
+    auto bits = [](uint64_t x) {
+        uint32_t b = 1;
+        while (b < 64 && (uint64_t(1) << b) <= x) ++b;
+        return b;
+    };
+    const uint32_t nb = bits(g->n - 1), bb = bits(2 * g->m), dbits = bits(g->max_degree);
+    if (nb + bb + dbits > 64) return false;
+    const uint32_t n = g->n;
+    DevBuf k0, k1, i0, i1, tmp;
+    cub::DoubleBuffer<uint32_t> keys(static_cast<uint32_t*>(k0.ensure(4 * size_t(n))),
+                                     static_cast<uint32_t*>(k1.ensure(4 * size_t(n))));
+    cub::DoubleBuffer<uint32_t> ids(static_cast<uint32_t*>(i0.ensure(4 * size_t(n))),
+                                    static_cast<uint32_t*>(i1.ensure(4 * size_t(n))));
+    const int blocks = int(std::min<uint32_t>((n + 255) / 256, uint32_t(g->sm_count) * 8));
+    hot_keys_kernel<<<blocks, 256>>>(g->d_csr, n, keys.Current(), ids.Current());
+    SABA_CUDA_CHECK(cudaGetLastError());
+    size_t tb = 0;
+    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, ids, int(n)));
+    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.ensure(tb), tb, keys, ids, int(n)));
+    g->rec_nb = nb;
+    g->rec_db = nb + bb;
+    g->d_rec = static_cast<uint64_t*>(pool_alloc(sizeof(uint64_t) * n));
+    g->d_rank = static_cast<uint32_t*>(pool_alloc(sizeof(uint32_t) * n));
+    rec_build_kernel<<<blocks, 256>>>(ids.Current(), g->d_csr, n, nb, g->rec_db, g->d_rec, g->d_rank);
+    SABA_CUDA_CHECK(cudaGetLastError());
+    const uint64_t words = (2 * g->m + 2) / 3;
+    g->d_adj_rank = static_cast<uint64_t*>(pool_alloc(sizeof(uint64_t) * (words ? words : 1)));
+    rank_adj_kernel<<<g->sm_count * 8, 256>>>(g->d_adj, g->d_rank, 2 * g->m, g->d_adj_rank);
+    SABA_CUDA_CHECK(cudaGetLastError());
+    SABA_CUDA_CHECK(cudaDeviceSynchronize());
+    return true;
+}
+
+template <int WPT, int T>
+bool launch_rec_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t L, uint64_t mult, void* counts,
+                  cudaStream_t st) {
+    auto k = walk_count_rec_kernel<WPT, T>;
+    const size_t smem = sizeof(uint32_t) * g->hot_count;
+    SABA_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int occ = 0;
+    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, T, smem));
+    if (occ < 1) return false;
+    const uint64_t blocks = uint64_t(g->sm_count) * occ;
+    const uint64_t per_round = blocks * T * WPT;
+    const uint64_t per_block = (nw + per_round - 1) / per_round * T * WPT;
+    if (per_block * L >= (uint64_t(1) << 32)) return false;  // shared uint32 counters
+    k<<<uint32_t(blocks), T, smem, st>>>(g->d_rec, g->d_rank, g->d_adj_rank, g->rec_nb, g->rec_db, g->hot_count,
+                                         keys, nw, L, mult, static_cast<unsigned long long*>(counts));
+    SABA_CUDA_CHECK(cudaGetLastError());
+    return true;
+}
 
 __global__ void add_counts_kernel(const uint32_t* __restrict__ c32, uint32_t n,
                                   unsigned long long* __restrict__ counts) {
@@ -513,6 +668,15 @@ void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, 
         return;
     }
     const bool packed = v.packed && g->d_adj_packed != nullptr;
+    if (v.rec == 1 && v.hot != 0 && v.packed && !c32 && ensure_rec(g)) {
+        bool ok = false;
+        switch (g->hot_threads) {
+            case 256: ok = launch_rec_t<4, 256>(g, keys, nw, L, mult, counts, st); break;
+            case 512: ok = launch_rec_t<4, 512>(g, keys, nw, L, mult, counts, st); break;
+            default: ok = launch_rec_t<4, 1024>(g, keys, nw, L, mult, counts, st); break;
+        }
+        if (ok) return;
+    }
     if (v.hot != 0 && !c32 && ensure_hot(g)) {
         const bool ok = packed ? (v.agg ? launch_hot_p<true, true>(g, keys, nw, L, mult, counts, st)
                                         : launch_hot_p<true, false>(g, keys, nw, L, mult, counts, st))

@@ -319,6 +319,9 @@ saba_cu_graph::~saba_cu_graph() {
     if (d_adj_fat16) saba_cu::pool_free(d_adj_fat16);
     if (d_csr_hot) saba_cu::pool_free(d_csr_hot);
     if (d_hot_vertex) saba_cu::pool_free(d_hot_vertex);
+    if (d_rec) saba_cu::pool_free(d_rec);
+    if (d_rank) saba_cu::pool_free(d_rank);
+    if (d_adj_rank) saba_cu::pool_free(d_adj_rank);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev2) cudaEventDestroy(ev2);

@@ -38,7 +38,8 @@ CAMPAIGN_MID = ["", "fat=1,wpt=2", "fat=1,wpt=8", "fat=1,agg=0",
                 "fat=0,hot=1,hthreads=512", "fat=0,hot=1,agg=0",
                 "fat=0,hot=0,wpt=1", "fat=0,hot=0,wpt=2", "fat=0,hot=0,wpt=8",
                 "fat=0,hot=0,packed=0", "fat=0,hot=0,agg=0", "c32=1", "c32=1,packed=0",
-                "sort=0", "sort=1", "fat=0,hot=1,sort=0"]
+                "sort=0", "sort=1", "fat=0,hot=1,sort=0",
+                "fat=0,rec=1", "fat=0,rec=1,hthreads=256", "fat=0,rec=0,hot=1", "fat=0,rec=1,sort=0"]
 CAMPAIGN_BIG = ["", "hot=0", "hot=1,hthreads=256", "hot=0,wpt=2", "c32=1", "fat=1", "sort=0"]
 AESC_ENV = [{}, {"SABA_AESC_FAT": "0"}, {"SABA_AESC_FAT16": "0"}, {"SABA_AESC_BITMAP": "0"},
             {"SABA_AESC_BITMAP": "1"}, {"SABA_AESC_WORKERS": "1"}, {"SABA_AESC_WORKERS": "2"},
@@ -84,6 +85,9 @@ def test_campaign_variants_mid_graph(sb, oracle, tmp_path):
     assert np.array_equal(got, want)
     spec = {"kind": "campaign", "graph": G_MID, "W": W, "L": L, "seed": seed, "hash": True, "shards": 2}
     got = run_variant(spec, {"SABA_WALK_VARIANT": "fat=0,hot=1"}, tmp_path, "mid_hash")["counts"]
+    assert np.array_equal(got, want)
+    spec = {"kind": "campaign", "graph": G_MID, "W": W, "L": L, "seed": seed, "shards": 3}
+    got = run_variant(spec, {"SABA_WALK_VARIANT": "fat=0,rec=1"}, tmp_path, "mid_rec_sh")["counts"]
     assert np.array_equal(got, want)
 
 
