@@ -76,6 +76,16 @@ int depths_per_graph() {
     return d;
 }
 
+// SABA_PULL_SKIP=0|1 forces the dense or the column-sparse pull (tuning
+// knob; -1 = decided per depth from the support degree sums)
+int pull_skip_force() {
+    static const int f = [] {
+        const char* e = getenv("SABA_PULL_SKIP");
+        return e ? atoi(e) : -1;
+    }();
+    return f;
+}
+
 struct AescState {
     uint32_t n_cap = 0;
     DevBuf P[2], Q[2], M[2], R;          // n x 64 doubles / uint64 masks / 64 x n rho
@@ -394,6 +404,70 @@ __device__ __forceinline__ void pull_range(const uint32_t* __restrict__ adj,
     }
 }
 
+// Column-sparse form of pull_range for depths where the columns' supports
+// cover a small part of the graph (shallow plans such as cfg5, tau~ ~ 2, whose
+// 64-source union frontier still goes dense): the 32 neighbour masks of a
+// chunk are gathered first (one per lane), then each lane reads Q[v] for its
+// two columns only when v is in the support of one of them. Rows outside a
+// column's support hold exact +0.0 there, so a skipped load adds nothing and
+// the sums are bit-identical to pull_range's.
+__device__ __forceinline__ void pull_range_skip(const uint32_t* __restrict__ adj,
+                                                const double* __restrict__ Qc,
+                                                const unsigned long long* __restrict__ Mc, uint32_t b,
+                                                uint32_t e, uint32_t lane, bool need, double& a0, double& a1,
+                                                unsigned long long& mask) {
+    constexpr int U = 4;  // the neighbour masks stay in registers: fewer Q loads in flight
+    const unsigned long long mine_bits = 3ull << (2 * lane);
+    for (uint32_t s0 = b; s0 < e; s0 += 32) {
+        const uint32_t cnt = min(32u, e - s0);
+        const uint32_t mine = lane < cnt ? adj[s0 + lane] : 0u;
+        const unsigned long long mine_mask = lane < cnt ? Mc[mine] : 0ull;
+        uint32_t k = 0;
+        for (; k + U <= cnt; k += U) {
+            double2 q[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const uint32_t v = __shfl_sync(0xffffffffu, mine, k + j);
+                const unsigned long long mm = __shfl_sync(0xffffffffu, mine_mask, k + j);
+                mask |= mm;
+                q[j] = need && (mm & mine_bits) ? reinterpret_cast<const double2*>(Qc + size_t(v) * kCols)[lane]
+                                                : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                a0 += q[j].x;
+                a1 += q[j].y;
+            }
+        }
+        for (; k < cnt; ++k) {
+            const uint32_t v = __shfl_sync(0xffffffffu, mine, k);
+            const unsigned long long mm = __shfl_sync(0xffffffffu, mine_mask, k);
+            mask |= mm;
+            const double2 q = need && (mm & mine_bits) ? reinterpret_cast<const double2*>(Qc + size_t(v) * kCols)[lane]
+                                                       : make_double2(0.0, 0.0);
+            a0 += q.x;
+            a1 += q.y;
+        }
+    }
+}
+
+// Column-sparse depth? The useful fraction of a dense pull's Q reads for
+// column c is degsum_c / 2m (the slots pointing into its support); below a
+// quarter on average over the active columns the mask-first form wins.
+// SABA_PULL_SKIP=0|1 forces either form (tuning knob; results identical).
+__device__ __forceinline__ bool columns_sparse(const unsigned long long* __restrict__ degsum_cur,
+                                               unsigned long long active, uint64_t two_m, int force) {
+    if (force >= 0) return force != 0;
+    unsigned long long tot = 0;
+    uint32_t na = 0;
+    for (int c = 0; c < kCols; ++c)
+        if ((active >> c) & 1ull) {
+            tot += degsum_cur[c];
+            ++na;
+        }
+    return tot * 4 < two_m * na;
+}
+
 // Write one finished row of depth l+1 (P, Q = P / d, support mask) and
 // account its degree into the support degree sums of its columns.
 __device__ __forceinline__ void pull_store(uint32_t x, uint32_t deg, double a0, double a1,
@@ -443,12 +517,16 @@ __global__ void __launch_bounds__(256, SABA_PULL_MINB)
               unsigned long long* __restrict__ ctrl, uint32_t n,
               const uint32_t* __restrict__ light_order, uint32_t nlight,
               const HeavyPiece* __restrict__ pieces, uint32_t npieces, double* __restrict__ part,
-              unsigned long long* __restrict__ part_mask) {
+              unsigned long long* __restrict__ part_mask, const unsigned long long* __restrict__ degsum_cur,
+              uint64_t two_m, int skip_force) {
     __shared__ unsigned long long bds[kCols];
+    __shared__ bool s_skip;
     const unsigned long long active = ctrl[kActive];
     if (!active) return;
     if (threadIdx.x < kCols) bds[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_skip = columns_sparse(degsum_cur, active, two_m, skip_force);
     __syncthreads();
+    const bool skip = s_skip;
     const bool dense = ctrl[kDense] != 0;
     const uint32_t lane = threadIdx.x & 31;
     const bool need = ((active >> (2 * lane)) & 3ull) != 0;
@@ -471,13 +549,19 @@ __global__ void __launch_bounds__(256, SABA_PULL_MINB)
             SABA_DCHECK(i < total);
             if (i < npieces) {
                 const HeavyPiece pc = pieces[i];
-                pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, need, a0, a1, mask);
+                if (skip)
+                    pull_range_skip(adj, Qc, Mc, pc.begin, pc.end, lane, need, a0, a1, mask);
+                else
+                    pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, need, a0, a1, mask);
                 reinterpret_cast<double2*>(part + size_t(i) * kCols)[lane] = make_double2(a0, a1);
                 if (lane == 0) part_mask[i] = mask;
             } else {
                 const uint32_t x = light_order[i - npieces];
                 const uint2 r = csr[x];
-                pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, need, a0, a1, mask);
+                if (skip)
+                    pull_range_skip(adj, Qc, Mc, r.x, r.x + r.y, lane, need, a0, a1, mask);
+                else
+                    pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, need, a0, a1, mask);
                 pull_store(x, r.y, a0, a1, mask, active, lane, Pn, Qn, Mn, ds0, ds1);
             }
             i = __shfl_sync(0xffffffffu, nxt, 0);
@@ -493,7 +577,10 @@ __global__ void __launch_bounds__(256, SABA_PULL_MINB)
         if (r.y > kHeavy) continue;  // pieces + combine
         double a0 = 0.0, a1 = 0.0;
         unsigned long long mask = 0;
-        pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, need, a0, a1, mask);
+        if (skip)
+            pull_range_skip(adj, Qc, Mc, r.x, r.x + r.y, lane, need, a0, a1, mask);
+        else
+            pull_range(adj, Qc, Mc, r.x, r.x + r.y, lane, need, a0, a1, mask);
         pull_store(x, r.y, a0, a1, mask, active, lane, Pn, Qn, Mn, ds0, ds1);
         if (lane == 0 && !dense) flag[x] = 0;
     }
@@ -509,11 +596,16 @@ __global__ void __launch_bounds__(256)
                      const uint32_t* __restrict__ adj, const double* __restrict__ Qc,
                      const unsigned long long* __restrict__ Mc, const uint32_t* __restrict__ flag,
                      double* __restrict__ part, unsigned long long* __restrict__ part_mask,
-                     const unsigned long long* __restrict__ ctrl, uint32_t dynamic) {
+                     const unsigned long long* __restrict__ ctrl, uint32_t dynamic,
+                     const unsigned long long* __restrict__ degsum_cur, uint64_t two_m, int skip_force) {
     const unsigned long long active = ctrl[kActive];
     if (!active) return;
     const bool dense = ctrl[kDense] != 0;
     if (dense && dynamic) return;  // aesc_pull takes the pieces in dense depths
+    __shared__ bool s_skip;
+    if (threadIdx.x == 0) s_skip = columns_sparse(degsum_cur, active, two_m, skip_force);
+    __syncthreads();
+    const bool skip = s_skip;
     const uint32_t lane = threadIdx.x & 31;
     const bool need = ((active >> (2 * lane)) & 3ull) != 0;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < npieces;
@@ -522,7 +614,10 @@ __global__ void __launch_bounds__(256)
         if (!dense && !flag[pc.row]) continue;
         double a0 = 0.0, a1 = 0.0;
         unsigned long long mask = 0;
-        pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, need, a0, a1, mask);
+        if (skip)
+            pull_range_skip(adj, Qc, Mc, pc.begin, pc.end, lane, need, a0, a1, mask);
+        else
+            pull_range(adj, Qc, Mc, pc.begin, pc.end, lane, need, a0, a1, mask);
         reinterpret_cast<double2*>(part + size_t(i) * kCols)[lane] = make_double2(a0, a1);
         if (lane == 0) part_mask[i] = mask;
     }
@@ -1280,12 +1375,13 @@ struct Engine {
                 aesc_pull_pieces<<<grid, 256, 0, s>>>(st->pieces.as<HeavyPiece>(), st->npieces, adj,
                                                       Q[cur], M[cur], flag, st->part.as<double>(),
                                                       st->part_mask.as<unsigned long long>(), ctrl,
-                                                      st->nlight);
+                                                      st->nlight, DS[cur], 2 * g->m, pull_skip_force());
             aesc_pull<<<grid_pull, 256, 0, s>>>(csr, adj, Q[cur], M[cur], P[cur ^ 1], Q[cur ^ 1], M[cur ^ 1],
                                            UL[cur ^ 1], UC + (cur ^ 1), flag, DS[cur ^ 1], ctrl, n,
                                            st->nlight ? st->light_order.as<uint32_t>() : nullptr, st->nlight,
                                            st->pieces.as<HeavyPiece>(), st->npieces, st->part.as<double>(),
-                                           st->part_mask.as<unsigned long long>());
+                                           st->part_mask.as<unsigned long long>(), DS[cur], 2 * g->m,
+                                           pull_skip_force());
             if (st->npieces)
                 aesc_pull_combine<<<grid_comb, 256, 0, s>>>(
                     st->heavy_rows.as<uint32_t>(), st->piece_off.as<uint32_t>(), st->nheavy, csr,

@@ -322,8 +322,8 @@ template <int WPT, int THREADS>
 __global__ void __launch_bounds__(THREADS)
     walk_count_rec_kernel(const uint64_t* __restrict__ rec, const uint32_t* __restrict__ rank,
                           const uint64_t* __restrict__ adj_rank, uint32_t nb, uint32_t db, uint32_t nhot,
-                          const uint64_t* __restrict__ keys, uint64_t nwalks, uint32_t L, uint64_t mult,
-                          unsigned long long* __restrict__ counts) {
+                          uint32_t l1_hot, const uint64_t* __restrict__ keys, uint64_t nwalks, uint32_t L,
+                          uint64_t mult, unsigned long long* __restrict__ counts) {
     extern __shared__ uint32_t hot_cnt[];
     for (uint32_t i = threadIdx.x; i < nhot; i += blockDim.x) hot_cnt[i] = 0;
     __syncthreads();
@@ -346,8 +346,14 @@ __global__ void __launch_bounds__(THREADS)
             const StepHash shs = step_hash(mult, l);
             uint64_t q[WPT];
 #pragma unroll
-            for (int r = 0; r < WPT; ++r)
-                q[r] = act[r] ? __ldg(reinterpret_cast<const unsigned long long*>(rec) + cur[r]) : 0ull;
+            for (int r = 0; r < WPT; ++r) {
+                // records of the l1_hot highest-degree vertices are cached in
+                // L1; the cold tail is read without L1 allocation so it does
+                // not evict them
+                q[r] = 0ull;
+                if (act[r]) q[r] = cur[r] < l1_hot ? __ldg(reinterpret_cast<const unsigned long long*>(rec) + cur[r])
+                                                   : ldg_na_u64(rec + cur[r]);
+            }
 #pragma unroll
             for (int r = 0; r < WPT; ++r) {
                 const uint32_t id = uint32_t(q[r] & idmask);
@@ -392,6 +398,7 @@ struct WalkVariant {
     int hot_count = 0;      // hub table entries (0 = as many as shared memory holds)
     int sort = -1;          // K1 SABA sort: 1 fused warp sort, 0 CUB segmented sort, -1 auto
     int rec = -1;           // degree-ranked records (walk_count_rec_kernel): 1 on, 0 off, -1 auto
+    int l1hot = -1;         // rec kernel: ranks whose records are L1-allocated (-1 = 12288)
 };
 
 WalkVariant walk_variant() {
@@ -414,6 +421,7 @@ WalkVariant walk_variant() {
             w.hot_count = get("hcount=", w.hot_count);
             w.sort = get("sort=", w.sort);
             w.rec = get("rec=", w.rec);
+            w.l1hot = get("l1hot=", w.l1hot);
         }
         return w;
     }();
@@ -562,8 +570,9 @@ bool launch_rec_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t 
     const uint64_t per_round = blocks * T * WPT;
     const uint64_t per_block = (nw + per_round - 1) / per_round * T * WPT;
     if (per_block * L >= (uint64_t(1) << 32)) return false;  // shared uint32 counters
+    const uint32_t l1_hot = walk_variant().l1hot >= 0 ? uint32_t(walk_variant().l1hot) : 12288u;
     k<<<uint32_t(blocks), T, smem, st>>>(g->d_rec, g->d_rank, g->d_adj_rank, g->rec_nb, g->rec_db, g->hot_count,
-                                         keys, nw, L, mult, static_cast<unsigned long long*>(counts));
+                                         l1_hot, keys, nw, L, mult, static_cast<unsigned long long*>(counts));
     SABA_CUDA_CHECK(cudaGetLastError());
     return true;
 }

@@ -46,6 +46,7 @@ AESC_ENV = [{}, {"SABA_AESC_FAT": "0"}, {"SABA_AESC_FAT16": "0"}, {"SABA_AESC_BI
             {"SABA_AESC_PRIO": "0"}, {"SABA_PULL_STATIC": "1"}, {"SABA_DEPTHS_PER_GRAPH": "2"},
             {"SABA_SHORT_STEPS": "0"}, {"SABA_SHORT_STEPS": "1000"},
             {"SABA_AESC_REC": "2"}, {"SABA_AESC_REC": "2", "SABA_SHORT_STEPS": "0"},
+            {"SABA_PULL_SKIP": "0"}, {"SABA_PULL_SKIP": "1"}, {"SABA_PULL_SKIP": "1", "SABA_PULL_STATIC": "1"},
             {"SABA_AESC_FAT": "0", "SABA_AESC_FAT16": "0", "SABA_AESC_REC": "0"},
             {"SABA_AESC_FAT": "0", "SABA_AESC_FAT16": "0", "SABA_AESC_REC": "0", "SABA_AESC_BITMAP": "1"}]
 
