@@ -202,7 +202,9 @@ SABA_API int saba_cu_rng_stream(saba_cu_graph* g, const uint32_t* starts, uint32
  * list; per bouquet step the distinct lane vertices are counted.
  * histogram_out[lanes+1], per_step_out[length-1] (distinct-access proxy,
  * bench.hpp:45-50), totals_out[4] = {total_distinct, samples, lane_steps,
- * degree_sum}. Unsharded; length > 1. */
+ * degree_sum}. length > 1. A shard (shard_index of shard_count) covers the
+ * start vertices v with v % shard_count == shard_index; the shards' outputs
+ * add up to the unsharded statistics exactly (integer sums). */
 SABA_API int saba_cu_branching_stats(saba_cu_graph* g, const saba_cu_campaign_config* cfg,
                                      uint64_t* histogram_out, uint64_t* per_step_out,
                                      uint64_t* totals_out);

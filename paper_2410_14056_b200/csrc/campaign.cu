@@ -712,7 +712,8 @@ __global__ void branch_stats_kernel(const uint2* __restrict__ csr, const uint32_
                                     const uint64_t* __restrict__ adjp_unused, uint32_t n,
                                     const uint32_t* __restrict__ kv, uint64_t k_uniform,
                                     uint32_t kpad, uint32_t L, uint32_t lanes, int sorted,
-                                    uint64_t master, uint64_t mult,
+                                    uint64_t master, uint64_t mult, uint32_t shard_index,
+                                    uint32_t shard_count,
                                     unsigned long long* __restrict__ hist,
                                     unsigned long long* __restrict__ per_step,
                                     unsigned long long* __restrict__ totals) {
@@ -722,7 +723,12 @@ __global__ void branch_stats_kernel(const uint2* __restrict__ csr, const uint32_
     uint32_t* seeds = reinterpret_cast<uint32_t*>(s_step + (L - 1));
     for (uint32_t i = threadIdx.x; i < lanes + 1 + (L - 1); i += blockDim.x) smem_u64[i] = 0;
     unsigned long long t_distinct = 0, t_samples = 0, t_lane_steps = 0, t_degsum = 0;
-    for (uint32_t v = blockIdx.x; v < n; v += gridDim.x) {
+    // Shards take start vertices in stripes (v mod shard_count): every bouquet
+    // belongs to one start vertex, so the shards' integer sums add up to the
+    // unsharded statistics exactly.
+    for (uint64_t vv = uint64_t(blockIdx.x) * shard_count + shard_index; vv < n;
+         vv += uint64_t(gridDim.x) * shard_count) {
+        const uint32_t v = uint32_t(vv);
         const uint32_t K = kv ? kv[v] : uint32_t(k_uniform);
         if (K == 0) continue;
         const uint64_t vseed = substream(master, v);
@@ -1073,7 +1079,6 @@ int saba_cu_branching_stats(saba_cu_graph* g, const saba_cu_campaign_config* cfg
         check_arg(g && cfg && histogram_out && per_step_out && totals_out, "null argument");
         validate_campaign(g, *cfg);
         check_arg(cfg->length > 1, "branching statistics need walks of length > 1");
-        check_arg(cfg->shard_count == 1, "branching statistics are computed unsharded");
         std::lock_guard<std::recursive_mutex> lock(g->mu);
         DeviceScope scope(g->device);
         const uint32_t n = g->n, L = cfg->length, lanes = cfg->lanes;
@@ -1103,11 +1108,13 @@ int saba_cu_branching_stats(saba_cu_graph* g, const saba_cu_campaign_config* cfg
         SABA_CUDA_CHECK(cudaMemset(hist, 0, sizeof(uint64_t) * (lanes + 1)));
         SABA_CUDA_CHECK(cudaMemset(step, 0, sizeof(uint64_t) * (L - 1)));
         SABA_CUDA_CHECK(cudaMemset(tot, 0, sizeof(uint64_t) * 4));
-        const int blocks = int(std::min<uint64_t>(n, uint64_t(g->sm_count) * 8));
+        const uint64_t nv = (uint64_t(n) + cfg->shard_count - 1) / cfg->shard_count;
+        const int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>(nv, uint64_t(g->sm_count) * 8)));
         branch_stats_kernel<<<blocks, 256, smem>>>(g->d_csr, g->d_adj, g->d_adj_packed, n, kv,
                                                    cfg->walks_per_vertex, kpad, L, lanes,
                                                    cfg->mode == SABA_MODE_SABA, cfg->master_seed,
-                                                   cfg->hash_multiplier, hist, step, tot);
+                                                   cfg->hash_multiplier, cfg->shard_index, cfg->shard_count,
+                                                   hist, step, tot);
         SABA_CUDA_CHECK(cudaGetLastError());
         SABA_CUDA_CHECK(cudaMemcpy(histogram_out, hist, sizeof(uint64_t) * (lanes + 1), cudaMemcpyDeviceToHost));
         SABA_CUDA_CHECK(cudaMemcpy(per_step_out, step, sizeof(uint64_t) * (L - 1), cudaMemcpyDeviceToHost));

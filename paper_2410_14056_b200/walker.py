@@ -291,17 +291,22 @@ def rng_stream(g: Graph, starts, walks_per_vertex: int = 1, length: int = 2,
     return words[: nw.value].astype("<u4").tobytes()
 
 
-def collect_branching(g: Graph, cfg: CampaignConfig, *, total_walks: int = 0, device: int = 0):
+def collect_branching(g: Graph, cfg: CampaignConfig, *, total_walks: int = 0, device: int = 0,
+                      shard_index: int = 0, shard_count: int = 1, raw: bool = False):
     """Branching statistics of the campaign's bouquets (walker.hpp:64-109,
     526-536) computed on the GPU (the reference's untimed stats pass,
-    bench.hpp:171-178)."""
+    bench.hpp:171-178). A shard covers the start vertices v with
+    v % shard_count == shard_index; with raw=True the integer arrays
+    (histogram, per_step, totals) come back so that shards can be summed."""
     hist = np.zeros(cfg.lanes + 1, np.uint64)
     step = np.zeros(cfg.length - 1, np.uint64)
     tot = np.zeros(4, np.uint64)
-    c = _cfg_c(cfg, total_walks, 0, 1)
+    c = _cfg_c(cfg, total_walks, shard_index, shard_count)
     L.check(L.lib().saba_cu_branching_stats(g.device_handle(device), C.byref(c), L.ptr(hist, L.u64p),
                                             L.ptr(step, L.u64p), L.ptr(tot, L.u64p)),
             "branching_stats")
+    if raw:
+        return hist, step, tot
     st = branching_stats(hist)
     st.mean_candidate_degree = float(tot[3]) / float(tot[2]) if tot[2] else 0.0
     return st, DistinctProxy(step, int(tot[0]))

@@ -189,6 +189,19 @@ def test_branching_statistics_match_reference(golden, sb):
     assert rep.branching.mean == 1.0 and rep.branching.p1 == 1 and rep.branching.p25 == 1
 
 
+def test_branching_statistics_shards_add_up(golden, sb):
+    """Vertex-striped shards of the statistics pass sum to the unsharded one."""
+    g = golden_graph(golden, "sf2000_8_17")
+    cfg = sb.CampaignConfig(walks_per_vertex=24, length=9, lanes=8, collect_stats=True)
+    for total in (0, 50_000):
+        whole = sb.collect_branching(g, cfg, total_walks=total, raw=True)
+        for S in (2, 5):
+            parts = [sb.collect_branching(g, cfg, total_walks=total, shard_index=i, shard_count=S, raw=True)
+                     for i in range(S)]
+            for k in range(3):
+                assert np.array_equal(sum(p[k] for p in parts), whole[k]), (total, S, k)
+
+
 def test_saba_clusters_bouquets(golden, sb):
     """test_walker.cpp:259-282: sorted seeds give fewer distinct lanes."""
     g = golden_graph(golden, "sf2000_8_17")
