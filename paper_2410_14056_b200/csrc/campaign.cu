@@ -243,6 +243,73 @@ __global__ void __launch_bounds__(kWalkThreads)
     }
 }
 
+// K2 over the fat adjacency with EVERY vertex's counter in shared memory
+// (graphs of up to ~80K vertices: 16-bit fields, smem_count16): a step is one
+// dependent gather and one shared-memory atomic, and no L2 reduction is left
+// on the step path. One block per SM; the block passes a barrier every
+// count16_steps() steps so that the 16-bit fields cannot carry (all warps of
+// a block run the same number of rounds and steps).
+template <int WPT, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+    walk_count_fat_priv_kernel(const uint2* __restrict__ csr, const uint64_t* __restrict__ fat,
+                               uint32_t idb, uint32_t sh, const uint64_t* __restrict__ keys,
+                               uint64_t nwalks, uint32_t L, uint64_t mult, uint32_t n,
+                               unsigned long long* __restrict__ counts) {
+    extern __shared__ uint32_t cnt16[];
+    const uint32_t words = (n + 1) / 2;
+    for (uint32_t i = threadIdx.x; i < words; i += THREADS) cnt16[i] = 0;
+    __syncthreads();
+    constexpr uint32_t kSync = count16_steps(THREADS, WPT);
+    static_assert(kSync >= 1, "block too large for 16-bit counters");
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (uint64_t(blockIdx.x) * THREADS + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * THREADS) >> 5;
+    const uint64_t per_round = nwarps * 32 * WPT;
+    const uint64_t rounds = (nwalks + per_round - 1) / per_round;
+    const uint64_t idmask = (uint64_t(1) << idb) - 1, bmask = (uint64_t(1) << (sh - idb)) - 1;
+    for (uint64_t round = 0; round < rounds; ++round) {
+        const uint64_t base = round * per_round + warp * 32 * WPT;
+        uint32_t cur[WPT], seed[WPT], sbase[WPT], deg[WPT];
+        bool act[WPT];
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {
+            const uint64_t i = base + uint64_t(r) * 32 + lane;
+            act[r] = i < nwalks;
+            const uint64_t k = act[r] ? __ldcs(reinterpret_cast<const unsigned long long*>(keys) + i) : 0;
+            cur[r] = uint32_t(k >> 32);
+            seed[r] = uint32_t(k);
+            const uint2 rec = act[r] ? ldg_csr(csr + cur[r]) : make_uint2(0, 1);
+            sbase[r] = rec.x;
+            deg[r] = rec.y;
+        }
+        for (uint32_t l = 1; l < L; ++l) {
+            const StepHash shs = step_hash(mult, l);
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) {
+                const uint32_t raw = seed[r] ^ hash_state_fast(shs, cur[r]);
+                const uint64_t f = act[r] ? __ldg(reinterpret_cast<const unsigned long long*>(fat) +
+                                                  sbase[r] + scaled_index(raw, deg[r]))
+                                          : 0ull;
+                cur[r] = uint32_t(f & idmask);
+                sbase[r] = uint32_t((f >> idb) & bmask);
+                deg[r] = uint32_t(f >> sh);
+            }
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) {
+                SABA_DCHECK(!act[r] || cur[r] < n);
+                if (act[r]) smem_count16(cnt16, cur[r], counts, cur[r]);
+            }
+            if (l % kSync == 0) __syncthreads();
+        }
+        __syncthreads();
+    }
+    for (uint32_t i = threadIdx.x; i < words; i += THREADS) {
+        const uint32_t w = cnt16[i];
+        if (w & 0xFFFFu) atomicAdd(counts + 2 * i, (unsigned long long)(w & 0xFFFFu));
+        if (w >> 16) atomicAdd(counts + 2 * i + 1, (unsigned long long)(w >> 16));
+    }
+}
+
 // K2 with hub-privatised counters. Visits are counted at DEPARTURE: the
 // record of x_{l-1} loaded at step l already says whether x_{l-1} is one of
 // the highest-degree vertices (field y >> shift), whose counters live in
@@ -280,11 +347,20 @@ __global__ void __launch_bounds__(THREADS)
             uint2 rec[WPT];
 #pragma unroll
             for (int r = 0; r < WPT; ++r) rec[r] = act[r] ? ldg_csr(csr_hot + cur[r]) : make_uint2(0, 0);
+            // the neighbour gathers of all WPT walks are issued before any
+            // of them is consumed; the visit of the departing vertex is
+            // counted while they are in flight
+            AdjWord<PACKED> nxt[WPT];
 #pragma unroll
             for (int r = 0; r < WPT; ++r) {
                 const uint32_t deg = rec[r].y & ((1u << shift) - 1);
-                const uint32_t slot = rec[r].y >> shift;
-                if (l >= 2) {  // count the departing vertex x_{l-1}
+                const uint32_t raw = seed[r] ^ hash_state_fast(shs, cur[r]);
+                nxt[r] = adj_load<PACKED>(adj, adjp, act[r] ? rec[r].x + scaled_index(raw, deg) : 0u);
+            }
+            if (l >= 2) {  // count the departing vertex x_{l-1}
+#pragma unroll
+                for (int r = 0; r < WPT; ++r) {
+                    const uint32_t slot = rec[r].y >> shift;
                     const bool hot = act[r] && slot != 0;
                     SABA_DCHECK(!hot || slot - 1 < nhot);
                     if (hot) atomicAdd(hot_cnt + (slot - 1), 1u);
@@ -293,9 +369,9 @@ __global__ void __launch_bounds__(THREADS)
                     else
                         count_visit(counts, cur[r], act[r] && !hot);
                 }
-                const uint32_t raw = seed[r] ^ hash_state_fast(shs, cur[r]);
-                cur[r] = act[r] ? adj_at<PACKED>(adj, adjp, rec[r].x + scaled_index(raw, deg)) : 0u;
             }
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) cur[r] = act[r] ? adj_id<PACKED>(nxt[r]) : 0u;
         }
 #pragma unroll
         for (int r = 0; r < WPT; ++r) {  // the last vertex x_{L-1}
@@ -311,27 +387,45 @@ __global__ void __launch_bounds__(THREADS)
 }
 
 // K2 over degree-ranked records (see saba_cu_graph::d_rec). A walk carries
-// the RANK r of its vertex: one 8-byte gather rec[r] yields the vertex id (for
-// the hash and the count), its base and its degree; the neighbour slot holds
-// the neighbour's rank. Records are laid out by descending degree, so the
-// records of the most visited vertices (a walk is at v with probability
-// ~ deg(v) / 2m) share a few KB of lines that stay in L1, and hubs are simply
-// r < nhot (their counters live in shared memory). Walks, selections and the
-// counted multiset are exactly those of walk_count_hot_kernel.
+// the RANK r of its vertex (descending degree): rec[r] = {id, base, degree} in
+// one uint64 and the neighbour slots hold ranks. A walk sits on v with
+// probability ~ deg(v) / 2m, so what the step path needs of the most visited
+// vertices is kept in shared memory for the whole launch:
+//   r < nrec: the record itself (no L2 request for the {base, degree} gather)
+//   r < ncnt: the visit counter, a 16-bit field (smem_count16; no L2 reduction)
+// K2 is bound by the SM's L1-miss request rate (~1 request per clock: one
+// each for the record, the neighbour slot and the visit reduction of a step),
+// so every request kept in shared memory is throughput. Walks, selections and
+// the counted multiset are exactly those of walk_count_hot_kernel: visits are
+// counted at departure, x_0 by the key generator, x_{L-1} after the loop.
+// One block per SM; all warps run the same rounds and steps and pass a
+// barrier every count16_steps() steps (see smem_count16).
 template <int WPT, int THREADS>
 __global__ void __launch_bounds__(THREADS)
-    walk_count_rec_kernel(const uint64_t* __restrict__ rec, const uint32_t* __restrict__ rank,
-                          const uint64_t* __restrict__ adj_rank, uint32_t nb, uint32_t db, uint32_t nhot,
-                          uint32_t l1_hot, const uint64_t* __restrict__ keys, uint64_t nwalks, uint32_t L,
-                          uint64_t mult, unsigned long long* __restrict__ counts) {
-    extern __shared__ uint32_t hot_cnt[];
-    for (uint32_t i = threadIdx.x; i < nhot; i += blockDim.x) hot_cnt[i] = 0;
+    walk_count_rank_kernel(const uint64_t* __restrict__ rec, const uint32_t* __restrict__ rank,
+                           const uint64_t* __restrict__ adj_rank, uint32_t nb, uint32_t db, uint32_t nrec,
+                           uint32_t ncnt, const uint64_t* __restrict__ keys, uint64_t nwalks, uint32_t L,
+                           uint64_t mult, unsigned long long* __restrict__ counts) {
+    extern __shared__ uint64_t rank_smem[];
+    uint64_t* rec_s = rank_smem;
+    uint32_t* cnt16 = reinterpret_cast<uint32_t*>(rank_smem + nrec);
+    const uint32_t cwords = (ncnt + 1) / 2;
+    for (uint32_t i = threadIdx.x; i < nrec; i += THREADS) rec_s[i] = rec[i];
+    for (uint32_t i = threadIdx.x; i < cwords; i += THREADS) cnt16[i] = 0;
     __syncthreads();
+    constexpr uint32_t kSync = count16_steps(THREADS, WPT);
+    static_assert(kSync >= 1, "block too large for 16-bit counters");
     const uint64_t idmask = (uint64_t(1) << nb) - 1, bmask = (uint64_t(1) << (db - nb)) - 1;
     const uint32_t lane = threadIdx.x & 31;
-    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-    for (uint64_t base = warp * 32 * WPT; base < nwalks; base += nwarps * 32 * WPT) {
+    const uint64_t warp = (uint64_t(blockIdx.x) * THREADS + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * THREADS) >> 5;
+    const uint64_t per_round = nwarps * 32 * WPT;
+    const uint64_t rounds = (nwalks + per_round - 1) / per_round;
+    auto record = [&](uint32_t r) {
+        return r < nrec ? rec_s[r] : __ldg(reinterpret_cast<const unsigned long long*>(rec) + r);
+    };
+    for (uint64_t round = 0; round < rounds; ++round) {
+        const uint64_t base = round * per_round + warp * 32 * WPT;
         uint32_t cur[WPT], seed[WPT];  // cur = rank of the walk's vertex
         bool act[WPT];
 #pragma unroll
@@ -346,43 +440,46 @@ __global__ void __launch_bounds__(THREADS)
             const StepHash shs = step_hash(mult, l);
             uint64_t q[WPT];
 #pragma unroll
-            for (int r = 0; r < WPT; ++r) {
-                // records of the l1_hot highest-degree vertices are cached in
-                // L1; the cold tail is read without L1 allocation so it does
-                // not evict them
-                q[r] = 0ull;
-                if (act[r]) q[r] = cur[r] < l1_hot ? __ldg(reinterpret_cast<const unsigned long long*>(rec) + cur[r])
-                                                   : ldg_na_u64(rec + cur[r]);
-            }
+            for (int r = 0; r < WPT; ++r) q[r] = act[r] ? record(cur[r]) : 0ull;
+            AdjWord<true> nxt[WPT];
 #pragma unroll
             for (int r = 0; r < WPT; ++r) {
                 const uint32_t id = uint32_t(q[r] & idmask);
                 const uint32_t sbase = uint32_t((q[r] >> nb) & bmask);
                 const uint32_t deg = uint32_t(q[r] >> db);
-                if (l >= 2) {  // count the departing vertex x_{l-1}
-                    const bool hot = act[r] && cur[r] < nhot;
-                    if (hot) atomicAdd(hot_cnt + cur[r], 1u);
+                SABA_DCHECK(!act[r] || deg > 0);
+                const uint32_t raw = seed[r] ^ hash_state_fast(shs, id);
+                nxt[r] = adj_load<true>(nullptr, adj_rank, act[r] ? sbase + scaled_index(raw, deg) : 0u);
+            }
+            if (l >= 2) {  // count the departing vertex x_{l-1} while the gathers are in flight
+#pragma unroll
+                for (int r = 0; r < WPT; ++r) {
+                    const uint32_t id = uint32_t(q[r] & idmask);
+                    const bool hot = act[r] && cur[r] < ncnt;
+                    if (hot) smem_count16(cnt16, cur[r], counts, id);
                     warp_count_visit(counts, id, act[r] && !hot, lane);
                 }
-                const uint32_t raw = seed[r] ^ hash_state_fast(shs, id);
-                cur[r] = act[r] ? adj_at<true>(nullptr, adj_rank, sbase + scaled_index(raw, deg)) : 0u;
-                SABA_DCHECK(!act[r] || deg > 0);
             }
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) cur[r] = act[r] ? adj_id<true>(nxt[r]) : 0u;
+            if (l % kSync == 0) __syncthreads();
         }
+        __syncthreads();
 #pragma unroll
         for (int r = 0; r < WPT; ++r) {  // the last vertex x_{L-1}
             const bool last = act[r] && L > 1;
-            const bool hot = last && cur[r] < nhot;
-            if (hot) atomicAdd(hot_cnt + cur[r], 1u);
-            const uint32_t id = last && !hot
-                                    ? uint32_t(__ldg(reinterpret_cast<const unsigned long long*>(rec) + cur[r]) & idmask)
-                                    : 0u;
+            const uint32_t id = last ? uint32_t(record(cur[r]) & idmask) : 0u;
+            const bool hot = last && cur[r] < ncnt;
+            if (hot) smem_count16(cnt16, cur[r], counts, id);
             warp_count_visit(counts, id, last && !hot, lane);
         }
+        __syncthreads();
     }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nhot; i += blockDim.x)
-        if (hot_cnt[i]) atomicAdd(counts + uint32_t(rec[i] & idmask), (unsigned long long)hot_cnt[i]);
+    for (uint32_t i = threadIdx.x; i < cwords; i += THREADS) {
+        const uint32_t w = cnt16[i];
+        if (w & 0xFFFFu) atomicAdd(counts + uint32_t(rec[2 * i] & idmask), (unsigned long long)(w & 0xFFFFu));
+        if (w >> 16) atomicAdd(counts + uint32_t(rec[2 * i + 1] & idmask), (unsigned long long)(w >> 16));
+    }
 }
 
 // Kernel variant (tuning knob; SABA_WALK_VARIANT="wpt=4,packed=1,c32=1,agg=1").
@@ -397,8 +494,10 @@ struct WalkVariant {
     int hot_threads = 1024; // block size of the hub-counter kernel (256, 512, 1024)
     int hot_count = 0;      // hub table entries (0 = as many as shared memory holds)
     int sort = -1;          // K1 SABA sort: 1 fused warp sort, 0 CUB segmented sort, -1 auto
-    int rec = -1;           // degree-ranked records (walk_count_rec_kernel): 1 on, 0 off, -1 auto
-    int l1hot = -1;         // rec kernel: ranks whose records are L1-allocated (-1 = 12288)
+    int rec = -1;           // degree-ranked records (walk_count_rank_kernel): 1 on, 0 off, -1 auto
+    int hrec = -1;          // rank kernel: records kept in shared memory (-1 = auto)
+    int hcnt = -1;          // rank kernel: 16-bit counters kept in shared memory (-1 = auto)
+    int priv = -1;          // fat kernel with all counters in shared memory (small graphs): 1/-1 on, 0 off
 };
 
 WalkVariant walk_variant() {
@@ -421,7 +520,9 @@ WalkVariant walk_variant() {
             w.hot_count = get("hcount=", w.hot_count);
             w.sort = get("sort=", w.sort);
             w.rec = get("rec=", w.rec);
-            w.l1hot = get("l1hot=", w.l1hot);
+            w.hrec = get("hrec=", w.hrec);
+            w.hcnt = get("hcnt=", w.hcnt);
+            w.priv = get("priv=", w.priv);
         }
         return w;
     }();
@@ -516,14 +617,14 @@ __global__ void rank_adj_kernel(const uint32_t* __restrict__ adj, const uint32_t
     }
 }
 
-// Degree-ranked records (walk_count_rec_kernel), built on the device once per
-// graph: the same stable descending-degree order as the hub table, so the hub
-// test r < hot_count picks exactly the hot kernel's hubs. Needs ranks that pack
-// into 21 bits and {id, base, degree} in 64 bits.
+// Degree-ranked records (walk_count_rank_kernel), built on the device once per
+// graph: a stable descending-degree order (ties by ascending id). Needs ranks
+// that pack into 21 bits and {id, base, degree} in 64 bits.
 bool ensure_rec(saba_cu_graph* g) {
     if (g->rec_tried) return g->d_rec != nullptr;
     g->rec_tried = true;
-    if (g->n == 0 || g->n > kPackMax || !ensure_hot(g)) return false;
+    if (g->n == 0 || g->n > kPackMax || g->m == 0) return false;
+    g->hot_threads = walk_variant().hot_threads;
     auto bits = [](uint64_t x) {
         uint32_t b = 1;
         while (b < 64 && (uint64_t(1) << b) <= x) ++b;
@@ -558,21 +659,27 @@ bool ensure_rec(saba_cu_graph* g) {
 }
 
 template <int WPT, int T>
-bool launch_rec_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t L, uint64_t mult, void* counts,
-                  cudaStream_t st) {
-    auto k = walk_count_rec_kernel<WPT, T>;
-    const size_t smem = sizeof(uint32_t) * g->hot_count;
+bool launch_rank_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t L, uint64_t mult, void* counts,
+                   cudaStream_t st) {
+    const WalkVariant v = walk_variant();
+    // 128 KB of shared memory (see ensure_hot on why not more): 3/8 for
+    // records (8 B each), 5/8 for 16-bit counters. A visit to rank r saves one
+    // L2 request through either table, so per byte a counter is worth four
+    // records; on cfg2 the sweep (profiles/r02_k2_rank_sweep.txt) has its
+    // minimum at 6,144 records + 40,960 counters.
+    const size_t budget = std::min<size_t>(size_t(128) << 10, g->smem_optin - 1024);
+    const uint32_t nrec = std::min<uint32_t>(g->n, v.hrec >= 0 ? uint32_t(v.hrec) : uint32_t(budget * 3 / 8 / 8));
+    const uint32_t ncnt = std::min<uint32_t>(g->n, v.hcnt >= 0 ? uint32_t(v.hcnt) : uint32_t(budget * 5 / 8 / 2));
+    const size_t smem = sizeof(uint64_t) * nrec + sizeof(uint32_t) * ((size_t(ncnt) + 1) / 2);
+    if (smem > g->smem_optin - 1024) return false;
+    auto k = walk_count_rank_kernel<WPT, T>;
     SABA_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int occ = 0;
     SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, T, smem));
     if (occ < 1) return false;
-    const uint64_t blocks = uint64_t(g->sm_count) * occ;
-    const uint64_t per_round = blocks * T * WPT;
-    const uint64_t per_block = (nw + per_round - 1) / per_round * T * WPT;
-    if (per_block * L >= (uint64_t(1) << 32)) return false;  // shared uint32 counters
-    const uint32_t l1_hot = walk_variant().l1hot >= 0 ? uint32_t(walk_variant().l1hot) : 12288u;
-    k<<<uint32_t(blocks), T, smem, st>>>(g->d_rec, g->d_rank, g->d_adj_rank, g->rec_nb, g->rec_db, g->hot_count,
-                                         l1_hot, keys, nw, L, mult, static_cast<unsigned long long*>(counts));
+    k<<<uint32_t(g->sm_count) * occ, T, smem, st>>>(g->d_rec, g->d_rank, g->d_adj_rank, g->rec_nb, g->rec_db, nrec,
+                                                    ncnt, keys, nw, L, mult,
+                                                    static_cast<unsigned long long*>(counts));
     SABA_CUDA_CHECK(cudaGetLastError());
     return true;
 }
@@ -626,6 +733,24 @@ void launch_fat_t(saba_cu_graph* g, int bps, const uint64_t* keys, uint64_t nw, 
     SABA_CUDA_CHECK(cudaGetLastError());
 }
 
+// all-vertex 16-bit counters: at most 160 KB of shared memory (see ensure_hot
+// on why the table must leave L1 room for the gathers in flight)
+constexpr uint32_t kPrivMaxVertices = (160u << 10) / 2;
+bool launch_fat_priv(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t L, uint64_t mult,
+                     void* counts, cudaStream_t st) {
+    constexpr int T = 1024, WPT = 4;
+    auto k = walk_count_fat_priv_kernel<WPT, T>;
+    const size_t smem = sizeof(uint32_t) * ((size_t(g->n) + 1) / 2);
+    SABA_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int occ = 0;
+    SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, T, smem));
+    if (occ < 1) return false;
+    k<<<uint32_t(g->sm_count) * occ, T, smem, st>>>(g->d_csr, g->d_adj_fat, g->fat_idb, g->fat_sh, keys, nw, L,
+                                                    mult, g->n, static_cast<unsigned long long*>(counts));
+    SABA_CUDA_CHECK(cudaGetLastError());
+    return true;
+}
+
 template <int WPT, bool P, bool A, int T>
 bool launch_hot_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t L, uint64_t mult,
                   void* counts, cudaStream_t st) {
@@ -666,6 +791,7 @@ void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, 
     // (cfg1: 24% faster fat, cfg2: 21% slower; profiles/r01_walk_variant_sweep2.txt)
     const bool want_fat = v.fat == 1 || (v.fat == -1 && 16 * g->m <= (uint64_t(48) << 20));
     if (want_fat && !c32 && ensure_fat(g)) {
+        if (v.priv != 0 && g->n <= kPrivMaxVertices && launch_fat_priv(g, keys, nw, L, mult, counts, st)) return;
         switch (v.wpt) {
             case 2: v.agg ? launch_fat_t<2, true>(g, v.blocks_per_sm, keys, nw, L, mult, counts, st)
                           : launch_fat_t<2, false>(g, v.blocks_per_sm, keys, nw, L, mult, counts, st); break;
@@ -677,13 +803,9 @@ void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, 
         return;
     }
     const bool packed = v.packed && g->d_adj_packed != nullptr;
-    if (v.rec == 1 && v.hot != 0 && v.packed && !c32 && ensure_rec(g)) {
-        bool ok = false;
-        switch (g->hot_threads) {
-            case 256: ok = launch_rec_t<4, 256>(g, keys, nw, L, mult, counts, st); break;
-            case 512: ok = launch_rec_t<4, 512>(g, keys, nw, L, mult, counts, st); break;
-            default: ok = launch_rec_t<4, 1024>(g, keys, nw, L, mult, counts, st); break;
-        }
+    if (v.rec != 0 && v.hot != 0 && v.packed && !c32 && ensure_rec(g)) {
+        const bool ok = g->hot_threads == 512 ? launch_rank_t<4, 512>(g, keys, nw, L, mult, counts, st)
+                                              : launch_rank_t<4, 1024>(g, keys, nw, L, mult, counts, st);
         if (ok) return;
     }
     if (v.hot != 0 && !c32 && ensure_hot(g)) {
@@ -1173,7 +1295,7 @@ int saba_cu_walk_campaign(saba_cu_graph* g, const saba_cu_campaign_config* cfg,
         for (auto& b : bufs) ptrs.push_back(b.p);
         reduce_to_root(reps, ptrs, g->n, ReduceType::U64, std::vector<cudaStream_t>(R, nullptr));
         DeviceScope scope(g->device);
-        SABA_CUDA_CHECK(cudaMemcpy(counts_out, bufs[0].p, sizeof(uint64_t) * g->n, cudaMemcpyDeviceToHost));
+        copy_d2h(counts_out, bufs[0].p, sizeof(uint64_t) * g->n, 0);  // staged through pinned buffers when large
         saba_cu_campaign_report r{};
         if (R == 1) {
             r.seconds = span_ms[0] * 1e-3;  // device events around the campaign

@@ -103,6 +103,9 @@ void ensure_pool(int device) {
     SABA_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t keep = UINT64_MAX;
     SABA_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    // SABA_L2_FETCH=32|64|128: DRAM -> L2 fetch granularity (tuning switch)
+    if (const char* e = getenv("SABA_L2_FETCH"))
+        SABA_CUDA_CHECK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(atoi(e))));
     done[device] = true;
 }
 
@@ -391,49 +394,61 @@ saba_cu_graph* create_replica(const uint32_t* offsets, const uint32_t* adjacency
         g->n = n;
         g->m = two_m / 2;
         lap("start");
+        // The uploads are enqueued first (asynchronous from pinned host
+        // memory); the host-side copy of the offsets and the degree scan run
+        // while they are in flight.
+        ensure_pool(device);
+        DevBuf d_offb, d_bad;
+        uint32_t* d_off = static_cast<uint32_t*>(d_offb.ensure(sizeof(uint32_t) * (size_t(n) + 1)));
+        unsigned int* bad = static_cast<unsigned int*>(d_bad.ensure(sizeof(unsigned int)));
+        g->d_csr = static_cast<uint2*>(pool_alloc_on(sizeof(uint2) * size_t(n), 0));
+        g->d_adj = static_cast<uint32_t*>(pool_alloc_on(sizeof(uint32_t) * (two_m ? two_m : 1), 0));
+        if (n <= kPackMax && two_m)
+            g->d_adj_packed = static_cast<uint64_t*>(pool_alloc_on(sizeof(uint64_t) * ((two_m + 2) / 3), 0));
+        SABA_CUDA_CHECK(cudaMemcpyAsync(d_off, offsets, sizeof(uint32_t) * (size_t(n) + 1),
+                                        cudaMemcpyHostToDevice, 0));
+        if (two_m)
+            SABA_CUDA_CHECK(cudaMemcpyAsync(g->d_adj, adjacency, sizeof(uint32_t) * two_m,
+                                            cudaMemcpyHostToDevice, 0));
+        pack_csr_kernel<<<(n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096, 256>>>(d_off, n, g->d_csr);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        SABA_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(unsigned int), 0));
+        check_ids_kernel<<<g->sm_count * 8, 256>>>(g->d_adj, two_m, n, bad);
+        SABA_CUDA_CHECK(cudaGetLastError());
+        if (g->d_adj_packed) {
+            pack_adj_kernel<<<g->sm_count * 8, 256>>>(g->d_adj, two_m, g->d_adj_packed);
+            SABA_CUDA_CHECK(cudaGetLastError());
+        }
+        if (trace) {
+            const auto T1 = std::chrono::steady_clock::now();
+            fprintf(stderr, "[saba] graph_create %-12s %8.3f ms\n", "enqueue",
+                    std::chrono::duration<double, std::milli>(T1 - T0).count());
+            T0 = T1;
+        }
         g->h_off.assign(offsets, offsets + n + 1);
-        lap("assign");
         uint32_t dmin = UINT32_MAX, dmax = 0;
+        bool monotone = true;
         for (uint32_t v = 0; v < n; ++v) {
-            check_data(offsets[v] <= offsets[v + 1], "offsets must be nondecreasing");
+            monotone &= offsets[v] <= offsets[v + 1];
             const uint32_t d = offsets[v + 1] - offsets[v];
             dmin = d < dmin ? d : dmin;
             dmax = d > dmax ? d : dmax;
         }
         g->min_degree = dmin;
         g->max_degree = dmax;
-        lap("host scan");
-
-        ensure_pool(device);
-        DevBuf d_offb, d_bad;
-        uint32_t* d_off = static_cast<uint32_t*>(d_offb.ensure(sizeof(uint32_t) * (size_t(n) + 1)));
-        unsigned int* bad = static_cast<unsigned int*>(d_bad.ensure(sizeof(unsigned int)));
-        g->d_csr = static_cast<uint2*>(pool_alloc(sizeof(uint2) * size_t(n)));
-        g->d_adj = static_cast<uint32_t*>(pool_alloc(sizeof(uint32_t) * (two_m ? two_m : 1)));
-        lap("alloc");
-        SABA_CUDA_CHECK(cudaMemcpy(d_off, offsets, sizeof(uint32_t) * (size_t(n) + 1),
-                                   cudaMemcpyHostToDevice));
-        if (two_m)
-            SABA_CUDA_CHECK(cudaMemcpy(g->d_adj, adjacency, sizeof(uint32_t) * two_m,
-                                       cudaMemcpyHostToDevice));
-        lap("h2d");
-        pack_csr_kernel<<<(n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096, 256>>>(d_off, n, g->d_csr);
-        SABA_CUDA_CHECK(cudaGetLastError());
-        SABA_CUDA_CHECK(cudaMemset(bad, 0, sizeof(unsigned int)));
-        check_ids_kernel<<<g->sm_count * 8, 256>>>(g->d_adj, two_m, n, bad);
-        SABA_CUDA_CHECK(cudaGetLastError());
+        if (trace) {
+            const auto T1 = std::chrono::steady_clock::now();
+            fprintf(stderr, "[saba] graph_create %-12s %8.3f ms\n", "host scan",
+                    std::chrono::duration<double, std::milli>(T1 - T0).count());
+            T0 = T1;
+        }
         unsigned int h_bad = 0;
         SABA_CUDA_CHECK(cudaMemcpy(&h_bad, bad, sizeof(h_bad), cudaMemcpyDeviceToHost));
-        check_data(h_bad == 0, "adjacency id out of range");
-        lap("check ids");
-        if (n <= kPackMax && two_m) {
-            const uint64_t words = (two_m + 2) / 3;
-            g->d_adj_packed = static_cast<uint64_t*>(pool_alloc(sizeof(uint64_t) * words));
-            pack_adj_kernel<<<g->sm_count * 8, 256>>>(g->d_adj, two_m, g->d_adj_packed);
-            SABA_CUDA_CHECK(cudaGetLastError());
-        }
         SABA_CUDA_CHECK(cudaDeviceSynchronize());
-        lap("pack");
+        lap("h2d + pack");
+        // the replica (and its unique_ptr) is released only after the device is idle
+        check_data(monotone, "offsets must be nondecreasing");
+        check_data(h_bad == 0, "adjacency id out of range");
         SABA_CUDA_CHECK(cudaEventCreate(&g->ev0));
         SABA_CUDA_CHECK(cudaEventCreate(&g->ev1));
         SABA_CUDA_CHECK(cudaEventCreate(&g->ev2));

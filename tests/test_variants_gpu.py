@@ -39,7 +39,9 @@ CAMPAIGN_MID = ["", "fat=1,wpt=2", "fat=1,wpt=8", "fat=1,agg=0",
                 "fat=0,hot=0,wpt=1", "fat=0,hot=0,wpt=2", "fat=0,hot=0,wpt=8",
                 "fat=0,hot=0,packed=0", "fat=0,hot=0,agg=0", "c32=1", "c32=1,packed=0",
                 "sort=0", "sort=1", "fat=0,hot=1,sort=0",
-                "fat=0,rec=1", "fat=0,rec=1,hthreads=256", "fat=0,rec=0,hot=1", "fat=0,rec=1,sort=0"]
+                "fat=0,rec=1", "fat=0,rec=1,hthreads=512", "fat=0,rec=0,hot=1", "fat=0,rec=1,sort=0",
+                "fat=0,rec=1,hrec=100,hcnt=301", "fat=0,rec=1,hrec=0,hcnt=0", "fat=0,rec=1,hrec=5000,hcnt=1000",
+                "fat=0,rec=1,hrec=0,hcnt=70000", "priv=0", "priv=1"]
 CAMPAIGN_BIG = ["", "hot=0", "hot=1,hthreads=256", "hot=0,wpt=2", "c32=1", "fat=1", "sort=0"]
 AESC_ENV = [{}, {"SABA_AESC_FAT": "0"}, {"SABA_AESC_FAT16": "0"}, {"SABA_AESC_BITMAP": "0"},
             {"SABA_AESC_BITMAP": "1"}, {"SABA_AESC_WORKERS": "1"}, {"SABA_AESC_WORKERS": "2"},
@@ -90,6 +92,21 @@ def test_campaign_variants_mid_graph(sb, oracle, tmp_path):
     spec = {"kind": "campaign", "graph": G_MID, "W": W, "L": L, "seed": seed, "shards": 3}
     got = run_variant(spec, {"SABA_WALK_VARIANT": "fat=0,rec=1"}, tmp_path, "mid_rec_sh")["counts"]
     assert np.array_equal(got, want)
+
+
+def test_campaign_16bit_counter_overflow(sb, oracle, tmp_path):
+    """The 16-bit shared-memory counters (smem_count16) of the all-vertex fat
+    kernel and of the rank kernel: a hub that takes about a quarter of all
+    visits crosses 2^15 many times in every block, so the guard-bit spill to
+    the global counter is exercised; counts stay bit-exact."""
+    G = ["star", 3000]
+    W, L, seed = 1 << 20, 48, 4
+    g, want = oracle_counts(sb, oracle, G, W, L, seed)
+    assert int(want[0]) > 148 * 65536  # every block's hub counter wraps its 15 bits more than once
+    for i, v in enumerate(["", "priv=0", "fat=0,rec=1", "fat=0,rec=1,hrec=1,hcnt=1", "fat=0,rec=0,hot=1"]):
+        spec = {"kind": "campaign", "graph": G, "W": W, "L": L, "seed": seed}
+        got = run_variant(spec, {"SABA_WALK_VARIANT": v} if v else {}, tmp_path, f"star{i}")["counts"]
+        assert np.array_equal(got, want), v
 
 
 def test_campaign_per_vertex_sort_paths(sb, oracle, tmp_path):

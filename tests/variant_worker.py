@@ -32,6 +32,12 @@ def make_graph(spec):
         ring = np.stack([a, (a + 1) % n], 1)
         extra = rng.integers(0, n, size=(chords, 2)).astype(np.uint32)
         return sb.Graph.from_edges(n, np.concatenate([ring, extra]))
+    if kind == "star":  # one hub next to every vertex of a ring: its counter overflows 16 bits in every block
+        n = spec[1]
+        a = np.arange(1, n, dtype=np.uint32)
+        hub = np.stack([np.zeros(n - 1, np.uint32), a], 1)
+        ring = np.stack([a, np.where(a + 1 < n, a + 1, 1).astype(np.uint32)], 1)
+        return sb.Graph.from_edges(n, np.concatenate([hub, ring]))
     raise ValueError(kind)
 
 

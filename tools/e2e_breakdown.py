@@ -12,7 +12,7 @@ import bench  # noqa: E402
 import paper_2410_14056_b200 as sb  # noqa: E402
 
 spec, walks, L = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "cfg2"]
-g = bench.make_graph(sb, spec)
+g = bench.make_graph(sb, spec, 0)
 cfg = sb.CampaignConfig(length=L, master_seed=bench.MASTER_SEED)
 ge = sb.Graph(torch.from_numpy(g.offsets).pin_memory().numpy(),
               torch.from_numpy(g.adjacency).pin_memory().numpy(), _trusted=True)
