@@ -351,7 +351,18 @@ def make_graph(sb, spec, device):
     return sb.make_chung_lu(spec[1], 2.2, 78.0, 30000.0, seed=GRAPH_SEED, keep_lcc=True, device=device)
 
 
-def walk_roofline(args, kern_ms, steps_per_rank, ms_per_step):
+K2_DESCR = {
+    "walk_count_rank_kernel": "walk_count_rank_kernel (degree-ranked records, packed rank adjacency; the top "
+                              "records and 16-bit visit counters in shared memory)",
+    "walk_count_hot_kernel": "walk_count_hot_kernel (packed adjacency, shared-memory hub counters)",
+    "walk_count_fat_priv_kernel": "walk_count_fat_priv_kernel (one fat gather per step; every vertex's 16-bit "
+                                  "counter in shared memory)",
+    "walk_count_fat_kernel": "walk_count_fat_kernel (one fat gather per step, L2 reductions)",
+    "walk_count_kernel": "walk_count_kernel (csr + neighbour gathers, L2 reductions)",
+}
+
+
+def walk_roofline(args, kern_ms, steps_per_rank, ms_per_step, kernel):
     peak, peak_src = read_peak()
     achieved = steps_per_rank * BYTES_PER_STEP / (kern_ms * 1e-3) / 1e9
     traffic = read_profile_json("ncu_traffic.json", args.workload)
@@ -362,17 +373,24 @@ def walk_roofline(args, kern_ms, steps_per_rank, ms_per_step):
             "bytes_per_step": BYTES_PER_STEP, "peak_source": peak_src,
             "model": "achieved = steps x 64 B (one 32 B sector for {base,deg} + one for the neighbour id, "
                      "SURVEY §8d) / K2 launch time (CUDA events on the launch stream)"}
+    roof["kernel"] = "K2 " + K2_DESCR.get(kernel, kernel)
     if args.workload == "cfg1":
         # the cfg1 CSR (4.5 MB) is L2-resident: HBM is not the bound, L2
         # random-sector throughput is (SURVEY §8d asks for it beside HBM)
-        l2 = achieved
-        roof["kernel"] = "K2 walk_count_fat_kernel (auto-selected: fat adjacency fits L2)"
+        # L2 sector bytes per step as ncu measured them on this kernel
+        # (profiles/ncu_traffic.json); without a capture, one 32 B sector per
+        # gather: the fat kernels take one gather per step, the others two
+        per_step = traffic.get("l2_sector_bytes_per_step") if isinstance(traffic, dict) else None
+        src = "ncu lts__t_sectors_srcunit_tex per step (profiles/ncu_traffic.json)"
+        if not per_step:
+            per_step = 32.0 if "fat" in kernel else 64.0
+            src = "algorithmic: one 32 B sector per gather"
+        l2 = steps_per_rank * per_step / (kern_ms * 1e-3) / 1e9
         roof["l2"] = {"achieved_sector_gbs": l2, "ceiling_gbs": L2_RANDOM_SECTOR_GBS,
-                      "frac": l2 / L2_RANDOM_SECTOR_GBS,
+                      "frac": l2 / L2_RANDOM_SECTOR_GBS, "sector_bytes_per_step": per_step,
+                      "sector_bytes_source": src,
                       "ceiling_source": "tools/gather_ceiling.cu random 32 B-sector gathers, 32 MB working "
                                         "set (profiles/r01_gather_ceiling.txt)"}
-    else:
-        roof["kernel"] = "K2 walk_count_hot_kernel (packed adjacency, shared-memory hub counters)"
     return roof
 
 
@@ -424,6 +442,7 @@ def run_ours(args):
             ends[i].record(stream)
             walk_ms.append(rep.walk_kernel_ms)
             launches += rep.launches
+            k2_kernel = rep.kernel
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -485,7 +504,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": walk_config(args.workload, g.n, g.m, world, args.dist_backend),
             "checksum": {"counts_sha256_16": counts_checksum(final), "total_visits": int(final.sum())},
-            "roofline": walk_roofline(args, kern_ms, steps_per_rank, ms_per_step),
+            "roofline": walk_roofline(args, kern_ms, steps_per_rank, ms_per_step, k2_kernel),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "steps/s",
                     "h2d_bytes_per_step": int(g.offsets.nbytes + g.adjacency.nbytes),

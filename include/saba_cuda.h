@@ -171,8 +171,14 @@ typedef struct {
     uint64_t shard_steps;  /* their steps */
     double walk_kernel_ms; /* K2 alone */
     uint32_t launches;     /* kernels launched by this call */
-    uint32_t reserved;
+    uint32_t kernel;       /* K2 variant that ran: SABA_K2_* */
 } saba_cu_campaign_report;
+#define SABA_K2_NONE 0     /* length 1: no steps */
+#define SABA_K2_GENERIC 1  /* walk_count_kernel: csr + neighbour gathers, L2 reductions */
+#define SABA_K2_FAT 2      /* walk_count_fat_kernel: one gather per step (L2-resident graphs) */
+#define SABA_K2_HOT 3      /* walk_count_hot_kernel: 32-bit hub counters in shared memory */
+#define SABA_K2_RANK 4     /* walk_count_rank_kernel: hub records + 16-bit hub counters in shared memory */
+#define SABA_K2_FAT_PRIV 5 /* walk_count_fat_priv_kernel: every counter in shared memory (small graphs) */
 
 /* Visit counts (VisitCountSink, walker.hpp:352-365) copied to host counts[n]. */
 SABA_API int saba_cu_walk_campaign(saba_cu_graph* g, const saba_cu_campaign_config* cfg,

@@ -36,7 +36,7 @@ class CampaignReportC(C.Structure):
     _fields_ = [("seconds", C.c_double), ("total_steps", C.c_uint64),
                 ("total_events", C.c_uint64), ("shard_walks", C.c_uint64),
                 ("shard_steps", C.c_uint64), ("walk_kernel_ms", C.c_double),
-                ("launches", C.c_uint32), ("reserved", C.c_uint32)]
+                ("launches", C.c_uint32), ("kernel", C.c_uint32)]
 
 
 class AescConfigC(C.Structure):

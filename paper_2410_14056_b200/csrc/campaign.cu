@@ -505,9 +505,10 @@ WalkVariant walk_variant() {
         WalkVariant w;
         if (const char* e = getenv("SABA_WALK_VARIANT")) {
             std::string s(e);
-            auto get = [&](const char* k, int def) {
-                const auto p = s.find(k);
-                return p == std::string::npos ? def : atoi(s.c_str() + p + strlen(k));
+            auto get = [&](const char* k, int def) {  // whole keys only: "rec=" must not match "hrec="
+                for (auto p = s.find(k); p != std::string::npos; p = s.find(k, p + 1))
+                    if (p == 0 || s[p - 1] == ',') return atoi(s.c_str() + p + strlen(k));
+                return def;
             };
             w.wpt = get("wpt=", w.wpt);
             w.packed = get("packed=", w.packed) != 0;
@@ -662,14 +663,15 @@ template <int WPT, int T>
 bool launch_rank_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t L, uint64_t mult, void* counts,
                    cudaStream_t st) {
     const WalkVariant v = walk_variant();
-    // 128 KB of shared memory (see ensure_hot on why not more): 3/8 for
-    // records (8 B each), 5/8 for 16-bit counters. A visit to rank r saves one
-    // L2 request through either table, so per byte a counter is worth four
-    // records; on cfg2 the sweep (profiles/r02_k2_rank_sweep.txt) has its
-    // minimum at 6,144 records + 40,960 counters.
-    const size_t budget = std::min<size_t>(size_t(128) << 10, g->smem_optin - 1024);
-    const uint32_t nrec = std::min<uint32_t>(g->n, v.hrec >= 0 ? uint32_t(v.hrec) : uint32_t(budget * 3 / 8 / 8));
-    const uint32_t ncnt = std::min<uint32_t>(g->n, v.hcnt >= 0 ? uint32_t(v.hcnt) : uint32_t(budget * 5 / 8 / 2));
+    // 63 KB of shared memory (the 64 KB carve-out; the rest of the SM's SRAM
+    // stays L1, which holds the lines of the gathers in flight): 20 KB of
+    // records, 43 KB of 16-bit counters. Counters come first: without them
+    // the reductions on the hottest vertices serialise in L2 (2,560 records +
+    // 22,016 counters: 17.3 ms on cfg2; 7,936 records and no counters: 45 ms;
+    // 128 KB split 6,144 / 40,960: 18.7 ms; profiles/r02_k2_rank_sweep.txt).
+    const size_t budget = std::min<size_t>(size_t(63) << 10, g->smem_optin - 1024);
+    const uint32_t nrec = std::min<uint32_t>(g->n, v.hrec >= 0 ? uint32_t(v.hrec) : uint32_t(budget * 20 / 63 / 8));
+    const uint32_t ncnt = std::min<uint32_t>(g->n, v.hcnt >= 0 ? uint32_t(v.hcnt) : uint32_t(budget * 43 / 63 / 2));
     const size_t smem = sizeof(uint64_t) * nrec + sizeof(uint32_t) * ((size_t(ncnt) + 1) / 2);
     if (smem > g->smem_optin - 1024) return false;
     auto k = walk_count_rank_kernel<WPT, T>;
@@ -791,7 +793,9 @@ void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, 
     // (cfg1: 24% faster fat, cfg2: 21% slower; profiles/r01_walk_variant_sweep2.txt)
     const bool want_fat = v.fat == 1 || (v.fat == -1 && 16 * g->m <= (uint64_t(48) << 20));
     if (want_fat && !c32 && ensure_fat(g)) {
+        g->last_k2 = SABA_K2_FAT_PRIV;
         if (v.priv != 0 && g->n <= kPrivMaxVertices && launch_fat_priv(g, keys, nw, L, mult, counts, st)) return;
+        g->last_k2 = SABA_K2_FAT;
         switch (v.wpt) {
             case 2: v.agg ? launch_fat_t<2, true>(g, v.blocks_per_sm, keys, nw, L, mult, counts, st)
                           : launch_fat_t<2, false>(g, v.blocks_per_sm, keys, nw, L, mult, counts, st); break;
@@ -806,6 +810,7 @@ void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, 
     if (v.rec != 0 && v.hot != 0 && v.packed && !c32 && ensure_rec(g)) {
         const bool ok = g->hot_threads == 512 ? launch_rank_t<4, 512>(g, keys, nw, L, mult, counts, st)
                                               : launch_rank_t<4, 1024>(g, keys, nw, L, mult, counts, st);
+        g->last_k2 = SABA_K2_RANK;
         if (ok) return;
     }
     if (v.hot != 0 && !c32 && ensure_hot(g)) {
@@ -813,8 +818,10 @@ void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, 
                                         : launch_hot_p<true, false>(g, keys, nw, L, mult, counts, st))
                                : (v.agg ? launch_hot_p<false, true>(g, keys, nw, L, mult, counts, st)
                                         : launch_hot_p<false, false>(g, keys, nw, L, mult, counts, st));
+        g->last_k2 = SABA_K2_HOT;
         if (ok) return;
     }
+    g->last_k2 = SABA_K2_GENERIC;
     switch (v.wpt) {
         case 1: launch_walk_w<1>(g, v, packed, c32, keys, nw, L, mult, counts, st); break;
         case 2: launch_walk_w<2>(g, v, packed, c32, keys, nw, L, mult, counts, st); break;
@@ -1083,6 +1090,7 @@ void fill_report(const saba_cu_graph* g, const saba_cu_campaign_config& c, uint6
     rep->total_events = total * c.length;
     rep->shard_walks = shard_walks;
     rep->shard_steps = shard_walks * (c.length - 1);
+    rep->kernel = c.length > 1 ? g->last_k2 : SABA_K2_NONE;
 }
 
 }  // namespace
@@ -1256,6 +1264,15 @@ int saba_cu_walk_campaign(saba_cu_graph* g, const saba_cu_campaign_config* cfg,
         // one combine of the integer counts on the first replica.
         const std::vector<saba_cu_graph*> reps = replicas_of(g);
         const uint32_t R = uint32_t(reps.size());
+        const bool trace = getenv("SABA_TRACE") != nullptr;
+        auto T0 = std::chrono::steady_clock::now();
+        auto lap = [&](const char* what) {
+            if (!trace) return;
+            const auto T1 = std::chrono::steady_clock::now();
+            fprintf(stderr, "[saba] campaign %-16s %8.3f ms\n", what,
+                    std::chrono::duration<double, std::milli>(T1 - T0).count());
+            T0 = T1;
+        };
         std::vector<DevBuf> bufs(R);
         std::vector<uint64_t> walks(R, 0);
         std::vector<float> walk_ms(R, 0.f), span_ms(R, 0.f);
@@ -1291,11 +1308,14 @@ int saba_cu_walk_campaign(saba_cu_graph* g, const saba_cu_campaign_config* cfg,
         for (auto& t : threads) t.join();
         for (auto& e : err)
             if (e) std::rethrow_exception(e);
+        lap("enqueue + wait");
         std::vector<void*> ptrs;
         for (auto& b : bufs) ptrs.push_back(b.p);
         reduce_to_root(reps, ptrs, g->n, ReduceType::U64, std::vector<cudaStream_t>(R, nullptr));
         DeviceScope scope(g->device);
+        lap("combine");
         copy_d2h(counts_out, bufs[0].p, sizeof(uint64_t) * g->n, 0);  // staged through pinned buffers when large
+        lap("counts d2h");
         saba_cu_campaign_report r{};
         if (R == 1) {
             r.seconds = span_ms[0] * 1e-3;  // device events around the campaign

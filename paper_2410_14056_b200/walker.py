@@ -228,8 +228,13 @@ class CampaignReport:
     walk_kernel_ms: float = 0.0
     launches: int = 0
     shard_walks: int = 0
+    kernel: str = ""  # K2 variant that ran (SABA_K2_* in include/saba_cuda.h)
     branching: BranchingStats | None = None
     proxy: DistinctProxy | None = None
+
+
+K2_KERNELS = {0: "", 1: "walk_count_kernel", 2: "walk_count_fat_kernel", 3: "walk_count_hot_kernel",
+              4: "walk_count_rank_kernel", 5: "walk_count_fat_priv_kernel"}
 
 
 def _cfg_c(cfg: CampaignConfig, total_walks: int, shard_index: int, shard_count: int):
@@ -240,7 +245,7 @@ def _cfg_c(cfg: CampaignConfig, total_walks: int, shard_index: int, shard_count:
 
 def _report(r: L.CampaignReportC) -> CampaignReport:
     return CampaignReport(r.seconds, r.total_steps, r.total_events, 1, False, r.walk_kernel_ms,
-                          r.launches, r.shard_walks)
+                          r.launches, r.shard_walks, K2_KERNELS.get(r.kernel, str(r.kernel)))
 
 
 def run_walk_campaign(g: Graph, cfg: CampaignConfig, sink: VisitCountSink, *,

@@ -1,22 +1,16 @@
-# round-2 GPU job 15: L2 fetch granularity / L2 prefetch-size loads on K2 (rank kernel), e2e breakdown with overlapped create
+# round-2 GPU job 18: rank kernel final sweep (parser fixed), ncu traffic + full capture of the default K2 on cfg2/cfg1, default bench
 set -x
 O=gpurun_out
-for f in "" 32 64 128; do
- for w in "" "hrec=6144,hcnt=40960" "rec=0"; do
-  echo "== cfg2 L2_FETCH=[$f] [$w]" >> $O/r02o_k2.txt
-  SABA_L2_FETCH=$f SABA_WALK_VARIANT=$w python tools/profile_campaign.py --reps 3 2>&1 | tail -2 >> $O/r02o_k2.txt
- done
+for w in "" "hrec=0,hcnt=31744" "hrec=0,hcnt=16384" "hrec=1024,hcnt=27648" "hrec=1536,hcnt=25600" "hrec=2048,hcnt=23552" "hrec=3072,hcnt=19968" "hrec=0,hcnt=15872" "hrec=2560,hcnt=22016,hthreads=512" ""; do
+  echo "== cfg2 [$w]" >> $O/r02r_k2.txt
+  SABA_WALK_VARIANT=$w python tools/profile_campaign.py --reps 3 2>&1 | tail -2 >> $O/r02r_k2.txt
 done
-for v in adjld6 adjld7 adjld8; do
-  export SABA_LIB=$PWD/paper_2410_14056_b200/_variants/$v/libsaba_cuda.so
-  echo "== $v" >> $O/r02o_k2.txt
-  python tools/profile_campaign.py --reps 3 | tail -2 >> $O/r02o_k2.txt
-done
-unset SABA_LIB
-cat $O/r02o_k2.txt
-SABA_TRACE=1 python tools/e2e_breakdown.py cfg2 > $O/r02o_e2e_breakdown.txt 2>&1; grep -v graph_build $O/r02o_e2e_breakdown.txt | tail -12
-M=lts__t_sectors_srcunit_tex_op_read.sum,lts__t_requests_srcunit_tex_op_read.sum,dram__bytes_read.sum,gpu__time_duration.sum,lts__t_sectors_srcunit_tex_op_read_lookup_miss.sum,lts__t_sectors_srcunit_tex_op_red.sum,l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum,l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum,l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed,lts__t_tag_requests.avg.pct_of_peak_sustained_elapsed,dram__throughput.avg.pct_of_peak_sustained_elapsed,l1tex__throughput.avg.pct_of_peak_sustained_elapsed
-for f in 64 128; do
-  SABA_L2_FETCH=$f python tools/profile_campaign.py --reps 2 > $O/r02o_plain_$f.log 2>&1 && \
-  SABA_L2_FETCH=$f ncu --metrics $M --clock-control none -k regex:walk_count -s 1 -c 1 --csv --log-file $O/r02o_ncu_f$f.csv python tools/profile_campaign.py --reps 2 > $O/r02o_ncu_$f.log 2>&1
-done
+cat $O/r02r_k2.txt
+M=dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sectors_srcunit_tex_op_write.sum,lts__t_sectors_srcunit_tex_op_red.sum,lts__t_sectors_srcunit_tex_op_atom.sum,gpu__time_duration.sum,lts__t_requests_srcunit_tex_op_read.sum,l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum,l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum,l1tex__data_pipe_lsu_wavefronts.sum
+python tools/profile_campaign.py --reps 2 > $O/r02r_plain_cfg2.log 2>&1 && \
+ncu --metrics $M --clock-control none -k regex:walk_count -s 1 -c 1 --csv --log-file $O/r02r_ncu_k2_cfg2.csv python tools/profile_campaign.py --reps 2 > $O/r02r_ncu_cfg2.log 2>&1
+python tools/profile_campaign.py --workload cfg1 --reps 2 > $O/r02r_plain_cfg1.log 2>&1 && \
+ncu --metrics $M --clock-control none -k regex:walk_count -s 1 -c 1 --csv --log-file $O/r02r_ncu_k2_cfg1.csv python tools/profile_campaign.py --workload cfg1 --reps 2 > $O/r02r_ncu_cfg1.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:walk_count -s 1 -c 1 -o $O/r02r_k2_full python tools/profile_campaign.py --reps 2 > $O/r02r_ncu_full.log 2>&1
+python bench.py > $O/r02r_bench_default.json 2> $O/r02r_bench_default.err; tail -c 1500 $O/r02r_bench_default.json
+python bench.py --workload cfg1 > $O/r02r_bench_cfg1.json 2> $O/r02r_bench_cfg1.err; tail -c 1200 $O/r02r_bench_cfg1.json
