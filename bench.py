@@ -455,6 +455,14 @@ def run_ours(args):
 
     final = counts.cpu().numpy().view(np.uint64).copy()
     assert int(final.sum()) == total_walks * L, (int(final.sum()), total_walks * L)
+    # share of all visits that fell on vertices whose counters sat in shared
+    # memory (the highest-degree ranks, ties by id, as the device orders them)
+    n_rec, n_cnt = sb.campaign_tables(g, dev_index)
+    deg = np.diff(g.offsets.astype(np.int64))
+    by_rank = np.argsort(-deg, kind="stable")
+    tables = {"records": n_rec, "counters": n_cnt,
+              "visits_on_shared_counters_frac": float(final[by_rank[:n_cnt]].sum()) / float(final.sum()),
+              "departures_from_shared_records_frac": float(final[by_rank[:n_rec]].sum()) / float(final.sum())}
 
     # end to end through the public API with host buffers (pinned CSR in,
     # host counts out); every step re-creates the device replica (H2D).
@@ -504,7 +512,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": walk_config(args.workload, g.n, g.m, world, args.dist_backend),
             "checksum": {"counts_sha256_16": counts_checksum(final), "total_visits": int(final.sum())},
-            "roofline": walk_roofline(args, kern_ms, steps_per_rank, ms_per_step, k2_kernel),
+            "roofline": dict(walk_roofline(args, kern_ms, steps_per_rank, ms_per_step, k2_kernel),
+                             shared_tables=tables),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "steps/s",
                     "h2d_bytes_per_step": int(g.offsets.nbytes + g.adjacency.nbytes),

@@ -192,6 +192,12 @@ SABA_API int saba_cu_walk_campaign_device(saba_cu_graph* g, const saba_cu_campai
                                  uint64_t* counts_dev, void* stream, int timing,
                                  saba_cu_campaign_report* report);
 
+/* Shared-memory tables of the handle's last campaign launch: how many of the
+ * highest-degree vertices had their {base, degree} record (records) and their
+ * visit counter (counters) on the SM. 0 / 0 for the kernels without tables.
+ * Diagnostic for bench lines (walker.hpp:352-365 has no counterpart). */
+SABA_API int saba_cu_campaign_tables(const saba_cu_graph* g, uint32_t* records, uint32_t* counters);
+
 /* rng_stream (stream.hpp:29-83): the raw 32-bit pre-selection words
  * seed ^ h(cur, l) of walks_per_vertex walks from each start, step-major per
  * start (walk k's word of step l at index (l-1)*K + k of its start's block).

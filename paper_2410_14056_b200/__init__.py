@@ -14,7 +14,7 @@ from .walker import (CampaignConfig, CampaignReport, HashSpec, SeedOrdering, See
                      gen_sorted_seeds, hash_state, mix64, random_bouquet, random_walk,
                      run_walk_campaign, run_walk_campaign_device, scaled_index, substream,
                      uniform_start_counts, walk_paths, campaign_shard_range, BranchingStats,
-                     DistinctProxy, branching_stats, collect_branching, rng_stream)
+                     DistinctProxy, branching_stats, collect_branching, rng_stream, campaign_tables)
 from .aesc import (AescConfig, CentralityEstimate, LandingProbs, TruncationPlan, aesc,
                    estimate_edge, propagate_landing_probabilities, truncated_lengths, walk_budget,
                    aesc_shard_sources, aesc_device, symmetrise,

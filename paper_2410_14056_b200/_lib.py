@@ -99,6 +99,7 @@ SIGNATURES = {
     "saba_cu_walk_campaign_device": (C.c_int, [vp, C.POINTER(CampaignConfigC), C.c_void_p,
                                                C.c_void_p, C.c_int,
                                                C.POINTER(CampaignReportC)]),
+    "saba_cu_campaign_tables": (C.c_int, [vp, u32p, u32p]),
     "saba_cu_branching_stats": (C.c_int, [vp, C.POINTER(CampaignConfigC), u64p, u64p, u64p]),
     "saba_cu_rng_stream": (C.c_int, [vp, u32p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int,
                                      C.c_uint64, C.c_uint64, u32p, u64p]),

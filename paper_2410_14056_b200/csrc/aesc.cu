@@ -1670,6 +1670,47 @@ void walk_dispatch(const Launch& L, bool fat, bool packed, bool f16) {
     }
 }
 
+// SABA_AESC_L2WIN (experiment): pin what the walk kernel gathers per vertex in
+// the persisting part of L2 while a chunk runs, so that the neighbour gathers
+// streaming through L2 cannot evict it. 1 = the rho columns of the chunk's
+// sources, 2 = the csr records. SABA_AESC_L2WIN_MB sizes the set-aside
+// (default: the device maximum); `share` = walk streams that hold a window.
+struct L2Window {
+    int mode = 0;
+    size_t setaside = 0, max_window = 0;
+};
+const L2Window& l2_window(int device) {
+    static L2Window w[64];
+    static std::once_flag once[64];
+    std::call_once(once[device], [&] {
+        const char* e = getenv("SABA_AESC_L2WIN");
+        L2Window& x = w[device];
+        x.mode = e ? atoi(e) : 0;
+        if (!x.mode) return;
+        int v = 0;
+        SABA_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, device));
+        x.setaside = size_t(v);
+        if (const char* m = getenv("SABA_AESC_L2WIN_MB")) x.setaside = std::min(x.setaside, size_t(atoi(m)) << 20);
+        SABA_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, device));
+        x.max_window = size_t(v);
+        SABA_CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, x.setaside));
+        if (getenv("SABA_TRACE"))
+            fprintf(stderr, "[saba] aesc L2 window mode %d: set-aside %zu MB, max window %zu MB\n", x.mode,
+                    x.setaside >> 20, x.max_window >> 20);
+    });
+    return w[device];
+}
+void set_l2_window(cudaStream_t s, const void* base, size_t bytes, const L2Window& w, int share) {
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    a.accessPolicyWindow.num_bytes = std::min(bytes, w.max_window);
+    a.accessPolicyWindow.hitRatio =
+        bytes ? std::min(1.0f, float(double(w.setaside) / double(share) / double(a.accessPolicyWindow.num_bytes))) : 0.f;
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    SABA_CUDA_CHECK(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a));
+}
+
 void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb, const double* R,
                const uint32_t* bits, uint64_t mult, double* g_hat_dev, uint32_t* launches,
                const uint4* recs = nullptr, float* walk_kernel_ms = nullptr) {
@@ -1701,6 +1742,24 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
         }();
         const bool short_walks = c.steps < short_steps * nw;
         const Launch L{out_g, out_w, nw, dg, g, R, bits, words, mult, score, s, recs};
+        const L2Window& lw = l2_window(g->device);
+        const bool windowed = lw.mode != 0 && !fat && !recs;
+        if (windowed) {
+            static const int share = [] {
+                const char* e = getenv("SABA_AESC_WORKERS");
+                return e && atoi(e) == 1 ? 1 : 2;
+            }();
+            if (lw.mode == 2) {
+                set_l2_window(s, g->d_csr, sizeof(uint2) * g->n, lw, share);
+            } else {
+                uint32_t lo = UINT32_MAX, hi = 0;
+                for (const WalkGroup& G : c.groups) {
+                    lo = std::min(lo, G.col);
+                    hi = std::max(hi, G.col);
+                }
+                set_l2_window(s, R + size_t(lo) * g->n, sizeof(double) * g->n * (size_t(hi) - lo + 1), lw, share);
+            }
+        }
         if (walk_kernel_ms) SABA_CUDA_CHECK(cudaEventRecord(st->ev_walk[0], s));
         if (short_walks)
             walk_dispatch<kShortWpt, kShortMinb>(L, fat, packed, f16);
@@ -1708,6 +1767,7 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
             walk_dispatch<4, 5>(L, fat, packed, false);
         SABA_CUDA_CHECK(cudaGetLastError());
         if (walk_kernel_ms) SABA_CUDA_CHECK(cudaEventRecord(st->ev_walk[1], s));
+        if (windowed) set_l2_window(s, nullptr, 0, lw, 1);
         aesc_pair_reduce<<<int(std::min<uint32_t>(nt, g->sm_count * 8)), 256, 0, s>>>(dt, nt, dg, score, part);
         SABA_CUDA_CHECK(cudaGetLastError());
         *launches += 2;

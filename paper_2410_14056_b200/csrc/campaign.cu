@@ -683,6 +683,8 @@ bool launch_rank_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t
                                                     ncnt, keys, nw, L, mult,
                                                     static_cast<unsigned long long*>(counts));
     SABA_CUDA_CHECK(cudaGetLastError());
+    g->last_nrec = nrec;
+    g->last_ncnt = ncnt;
     return true;
 }
 
@@ -750,6 +752,8 @@ bool launch_fat_priv(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32
     k<<<uint32_t(g->sm_count) * occ, T, smem, st>>>(g->d_csr, g->d_adj_fat, g->fat_idb, g->fat_sh, keys, nw, L,
                                                     mult, g->n, static_cast<unsigned long long*>(counts));
     SABA_CUDA_CHECK(cudaGetLastError());
+    g->last_nrec = 0;
+    g->last_ncnt = g->n;
     return true;
 }
 
@@ -772,6 +776,8 @@ bool launch_hot_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t 
                                          g->hot_count, g->hot_shift, keys, nw, L, mult,
                                          static_cast<unsigned long long*>(counts));
     SABA_CUDA_CHECK(cudaGetLastError());
+    g->last_nrec = 0;
+    g->last_ncnt = g->hot_count;
     return true;
 }
 
@@ -788,6 +794,7 @@ bool launch_hot_p(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t 
 void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, uint32_t L,
                  uint64_t mult, void* counts, cudaStream_t st) {
     const WalkVariant v = walk_variant();
+    g->last_nrec = g->last_ncnt = 0;
     // auto: the fat array (8 B/slot) pays off while it stays L2-resident;
     // beyond that the packed 2.67 B/slot adjacency moves fewer DRAM bytes
     // (cfg1: 24% faster fat, cfg2: 21% slower; profiles/r01_walk_variant_sweep2.txt)
@@ -1171,6 +1178,14 @@ int saba_cu_walk_paths(saba_cu_graph* g, const uint32_t* starts, const uint32_t*
         SABA_CUDA_CHECK(cudaGetLastError());
         SABA_CUDA_CHECK(cudaMemcpy(paths_out, d_p.p, sizeof(uint32_t) * count * length,
                                    cudaMemcpyDeviceToHost));
+    });
+}
+
+int saba_cu_campaign_tables(const saba_cu_graph* g, uint32_t* records, uint32_t* counters) {
+    return guard([&] {
+        check_arg(g && records && counters, "null argument");
+        *records = g->last_nrec;
+        *counters = g->last_ncnt;
     });
 }
 

@@ -134,6 +134,7 @@ struct saba_cu_graph {
     uint32_t rec_nb = 0, rec_db = 0;
     bool rec_tried = false;
     uint32_t last_k2 = 0;  // SABA_K2_* of the last campaign launch (reported)
+    uint32_t last_nrec = 0, last_ncnt = 0;  // its shared-memory tables (saba_cu_campaign_tables)
     uint32_t hot_shift = 18;  // degree bits below the slot field (fits max_degree)
     int hot_threads = 1024;   // block size the hot table was sized for
     bool hot_tried = false;

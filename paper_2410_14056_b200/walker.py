@@ -331,6 +331,14 @@ def run_walk_campaign_device(g: Graph, cfg: CampaignConfig, counts_dev_ptr: int,
     return _report(rep)
 
 
+def campaign_tables(g: Graph, device: int = 0):
+    """(records, counters): how many of the highest-degree vertices had their
+    record / visit counter in shared memory in the handle's last campaign."""
+    r, c = C.c_uint32(0), C.c_uint32(0)
+    L.check(L.lib().saba_cu_campaign_tables(g.device_handle(device), C.byref(r), C.byref(c)), "campaign_tables")
+    return int(r.value), int(c.value)
+
+
 def uniform_start_counts(n: int, total_walks: int, master_seed: int = 42) -> np.ndarray:
     """K_v of the uniform-start campaign (host restatement for bookkeeping)."""
     s = substream(master_seed, START_TAG)

@@ -211,3 +211,27 @@ def test_saba_clusters_bouquets(golden, sb):
     h, s = run(sb.WalkMode.Hash), run(sb.WalkMode.Saba)
     assert s.branching.mean < h.branching.mean
     assert s.proxy.per_step[0] <= h.proxy.per_step[0]
+
+
+def test_campaign_report_names_the_kernel(sb, oracle):
+    """The campaign report says which K2 variant ran (saba_cuda.h SABA_K2_*):
+    a small graph takes the all-vertex shared-counter kernel, a graph beyond
+    the fat adjacency's L2 budget the degree-ranked one, and a length-1
+    campaign launches no walk kernel. Counts stay the oracle's either way."""
+    small = sb.make_rmat(12, 8, seed=5)
+    sink = sb.VisitCountSink(small.n)
+    rep = sb.run_walk_campaign(small, sb.CampaignConfig(length=9, master_seed=2), sink, total_walks=20000)
+    assert rep.kernel == "walk_count_fat_priv_kernel"
+    kv = oracle.uniform_start_counts(small.n, 20000, 2)
+    assert np.array_equal(sink.counts, oracle.campaign_counts(small.offsets, small.adjacency, length=9, master=2,
+                                                              k_per_vertex=kv))
+    sink1 = sb.VisitCountSink(small.n)
+    rep1 = sb.run_walk_campaign(small, sb.CampaignConfig(length=1, master_seed=2), sink1, total_walks=20000)
+    assert rep1.kernel == "" and int(sink1.counts.sum()) == 20000
+    big = sb.make_chung_lu(300_000, 2.2, 24.0, 3000.0, seed=2)  # 16 m > 48 MiB: no fat adjacency
+    sinkb = sb.VisitCountSink(big.n)
+    repb = sb.run_walk_campaign(big, sb.CampaignConfig(length=17, master_seed=6), sinkb, total_walks=300000)
+    assert repb.kernel == "walk_count_rank_kernel"
+    kvb = oracle.uniform_start_counts(big.n, 300000, 6)
+    assert np.array_equal(sinkb.counts, oracle.campaign_counts(big.offsets, big.adjacency, length=17, master=6,
+                                                               k_per_vertex=kvb))

@@ -44,6 +44,7 @@ for r in rows[1:]:
 n = max(len(launches), 1)
 dram = per.get("dram__bytes_read.sum", 0.0) + per.get("dram__bytes_write.sum", 0.0)
 l2 = sum(v for k, v in per.items() if k.startswith("lts__t_sectors_srcunit_tex")) * 32
+red = per.get("lts__t_sectors_srcunit_tex_op_red.sum", 0.0) + per.get("lts__t_sectors_srcunit_tex_op_atom.sum", 0.0)
 t = per.get("gpu__time_duration.sum", 0.0)
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 try:
@@ -51,6 +52,7 @@ try:
 except OSError:
     srchash = None
 entry = {f"dram_bytes_per_{a.unit_name}": dram / a.units, f"l2_sector_bytes_per_{a.unit_name}": l2 / a.units,
+         f"l2_reductions_per_{a.unit_name}": red / a.units, "l2_reductions_per_launch": red / n,
          "dram_bytes_per_launch": dram / n, "l2_sector_bytes_per_launch": l2 / n, "launches": len(launches),
          "units": a.units, "ncu_seconds_total": t, "kernel_regex": a.kernel, "csv": os.path.basename(a.csv),
          "srchash": srchash, "note": a.note or "ncu --clock-control none, serialised cold-ish launches"}
