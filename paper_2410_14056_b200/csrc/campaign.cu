@@ -532,10 +532,10 @@ WalkVariant walk_variant() {
 
 // The top vertices by degree get a shared-memory counter slot, packed into
 // the spare high bits of the degree field (hot_shift = bits of max degree).
-__global__ void hot_keys_kernel(const uint2* __restrict__ csr, uint32_t n, uint32_t* __restrict__ key,
-                                uint32_t* __restrict__ id) {
+__global__ void hot_keys_kernel(const uint2* __restrict__ csr, uint32_t n, uint32_t dmax,
+                                uint32_t* __restrict__ key, uint32_t* __restrict__ id) {
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        key[v] = ~csr[v].y;  // ascending sort = descending degree
+        key[v] = dmax - csr[v].y;  // ascending sort = descending degree; keys fit bits(dmax)
         id[v] = v;
     }
 }
@@ -578,11 +578,13 @@ bool ensure_hot(saba_cu_graph* g) {
     cub::DoubleBuffer<uint32_t> ids(static_cast<uint32_t*>(i0.ensure(4 * size_t(n))),
                                     static_cast<uint32_t*>(i1.ensure(4 * size_t(n))));
     const int blocks = int(std::min<uint32_t>((n + 255) / 256, uint32_t(g->sm_count) * 8));
-    hot_keys_kernel<<<blocks, 256>>>(g->d_csr, n, keys.Current(), ids.Current());
+    hot_keys_kernel<<<blocks, 256>>>(g->d_csr, n, g->max_degree, keys.Current(), ids.Current());
     SABA_CUDA_CHECK(cudaGetLastError());
     size_t tb = 0;
-    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, ids, int(n)));
-    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.ensure(tb), tb, keys, ids, int(n)));
+    int key_bits = 1;  // radix passes only over the bits a degree can set
+    while (key_bits < 32 && (g->max_degree >> key_bits) != 0) ++key_bits;
+    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, ids, int(n), 0, key_bits));
+    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.ensure(tb), tb, keys, ids, int(n), 0, key_bits));
     g->d_csr_hot = static_cast<uint2*>(pool_alloc(sizeof(uint2) * n));
     g->d_hot_vertex = static_cast<uint32_t*>(pool_alloc(sizeof(uint32_t) * h));
     SABA_CUDA_CHECK(cudaMemcpy(g->d_csr_hot, g->d_csr, sizeof(uint2) * n, cudaMemcpyDeviceToDevice));
@@ -640,11 +642,13 @@ bool ensure_rec(saba_cu_graph* g) {
     cub::DoubleBuffer<uint32_t> ids(static_cast<uint32_t*>(i0.ensure(4 * size_t(n))),
                                     static_cast<uint32_t*>(i1.ensure(4 * size_t(n))));
     const int blocks = int(std::min<uint32_t>((n + 255) / 256, uint32_t(g->sm_count) * 8));
-    hot_keys_kernel<<<blocks, 256>>>(g->d_csr, n, keys.Current(), ids.Current());
+    hot_keys_kernel<<<blocks, 256>>>(g->d_csr, n, g->max_degree, keys.Current(), ids.Current());
     SABA_CUDA_CHECK(cudaGetLastError());
     size_t tb = 0;
-    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, ids, int(n)));
-    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.ensure(tb), tb, keys, ids, int(n)));
+    int key_bits = 1;  // radix passes only over the bits a degree can set
+    while (key_bits < 32 && (g->max_degree >> key_bits) != 0) ++key_bits;
+    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, ids, int(n), 0, key_bits));
+    SABA_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.ensure(tb), tb, keys, ids, int(n), 0, key_bits));
     g->rec_nb = nb;
     g->rec_db = nb + bb;
     g->d_rec = static_cast<uint64_t*>(pool_alloc(sizeof(uint64_t) * n));

@@ -159,7 +159,7 @@ bool is_pinned(const void* p) {
 }
 
 void par_memcpy(void* dst, const void* src, size_t bytes) {
-    constexpr size_t kPiece = size_t(1) << 20;
+    constexpr size_t kPiece = size_t(256) << 10;  // small pieces: first-touch page faults spread over the threads
     const int64_t pieces = int64_t((bytes + kPiece - 1) / kPiece);
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < pieces; ++i) {
