@@ -1,20 +1,29 @@
 // Bouquets walk campaigns on sm_100a.
 //
-//   K1a start_hist_kernel   uniform-random starts: K_v histogram
-//   K1b CUB scan            K_v -> walk-list offsets
-//   K1c gen_keys_kernel     per-vertex walk seeds counter_hash(vseed,k)>>32
-//                           (walker.hpp:437-438) as keys (v<<32 | seed), plus
-//                           the step-0 visit of every walk (walker.hpp:216-220)
-//   K1d CUB segmented sort  SABA: seeds sorted within each start vertex
-//                           (walker.hpp:439) -> a warp is a 32-lane bouquet
-//   K2  walk_count_kernel   L-1 lockstep hashed steps per lane
-//                           (walker.hpp:221-235) + VisitCountSink epilogue
-//                           (walker.hpp:355) as warp-aggregated L2 reductions;
-//                           the default walk_count_hot_kernel counts visits at
-//                           departure and keeps the ~32K highest-degree
-//                           vertices' counters in shared memory (one
-//                           1024-thread block per SM), walk_count_fat_kernel
-//                           takes one gather per step on L2-resident graphs
+//   K1a start_hist_kernel       uniform-random starts: K_v histogram
+//   K1b CUB scan                K_v -> walk-list offsets
+//   K1c gen_sorted_keys_kernel  per-vertex walk seeds counter_hash(vseed,k)>>32
+//                               (walker.hpp:437-438) as keys (v<<32 | seed),
+//                               sorted within each start vertex by the warp
+//                               that generates them (SABA, walker.hpp:439: a
+//                               warp is a 32-lane bouquet), plus the step-0
+//                               visit of every walk (walker.hpp:216-220);
+//                               gen_keys_kernel + CUB segmented sort for large
+//                               per-vertex campaigns
+//   K2  L-1 lockstep hashed steps per lane (walker.hpp:221-235) + the
+//       VisitCountSink epilogue (walker.hpp:355); launch_walk picks
+//       walk_count_rank_kernel      default up to 2^21 vertices: degree-ranked
+//                                   records, the top records and 16-bit visit
+//                                   counters in shared memory, the rest as
+//                                   warp-aggregated L2 reductions
+//       walk_count_fat_priv_kernel  L2-resident graphs of <= 80K vertices: one
+//                                   fat gather per step, every counter in
+//                                   shared memory
+//       walk_count_fat_kernel       other L2-resident graphs
+//       walk_count_hot_kernel       beyond 2^21 vertices: 32-bit hub counters
+//                                   in shared memory (one 1024-thread block
+//                                   per SM), visits counted at departure
+//       walk_count_kernel           generic fallback (and uint32 counters)
 //
 // A GPU bouquet is a warp: lanes hold consecutive entries of the sorted key
 // array, so they share their start vertex and hold adjacent seeds — the

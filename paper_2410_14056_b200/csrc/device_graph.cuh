@@ -123,11 +123,12 @@ struct saba_cu_graph {
     uint2* d_csr_hot = nullptr;
     uint32_t* d_hot_vertex = nullptr;  // slot -> vertex
     uint32_t hot_count = 0;
-    // Degree-ranked walk records (campaign K2 "rec" variant): vertex of rank r
+    // Degree-ranked walk records (walk_count_rank_kernel): vertex of rank r
     // (descending degree, ties by id) has rec[r] = id | base << rec_nb |
     // degree << rec_db in one uint64, and the adjacency is restated in rank
-    // space (same slot order). The hottest records sit together at the front,
-    // so they stay in L1, and the hub test is r < hot_count.
+    // space (same slot order). The kernel keeps the first records and the
+    // visit counters of the first ranks in shared memory: hub tests are
+    // plain comparisons of the rank.
     uint64_t* d_rec = nullptr;
     uint32_t* d_rank = nullptr;      // vertex id -> rank
     uint64_t* d_adj_rank = nullptr;  // 3 x 21-bit ranks per uint64 (n <= 2^21)
