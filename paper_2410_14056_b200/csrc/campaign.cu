@@ -308,7 +308,9 @@ __global__ void __launch_bounds__(THREADS)
                 SABA_DCHECK(!act[r] || cur[r] < n);
                 if (act[r]) smem_count16(cnt16, cur[r], counts, cur[r]);
             }
+#ifndef SABA_COUNT16_NOSYNC  // measurement builds only: without the barrier the 16-bit fields may carry
             if (l % kSync == 0) __syncthreads();
+#endif
         }
         __syncthreads();
     }
@@ -409,12 +411,12 @@ __global__ void __launch_bounds__(THREADS)
 // counted at departure, x_0 by the key generator, x_{L-1} after the loop.
 // One block per SM; all warps run the same rounds and steps and pass a
 // barrier every count16_steps() steps (see smem_count16).
-template <int WPT, int THREADS>
+template <int WPT, int THREADS, class CT>
 __global__ void __launch_bounds__(THREADS)
     walk_count_rank_kernel(const uint64_t* __restrict__ rec, const uint32_t* __restrict__ rank,
                            const uint64_t* __restrict__ adj_rank, uint32_t nb, uint32_t db, uint32_t nrec,
                            uint32_t ncnt, const uint64_t* __restrict__ keys, uint64_t nwalks, uint32_t L,
-                           uint64_t mult, unsigned long long* __restrict__ counts) {
+                           uint64_t mult, CT* __restrict__ counts) {
     extern __shared__ uint64_t rank_smem[];
     uint64_t* rec_s = rank_smem;
     uint32_t* cnt16 = reinterpret_cast<uint32_t*>(rank_smem + nrec);
@@ -471,7 +473,9 @@ __global__ void __launch_bounds__(THREADS)
             }
 #pragma unroll
             for (int r = 0; r < WPT; ++r) cur[r] = act[r] ? adj_id<true>(nxt[r]) : 0u;
+#ifndef SABA_COUNT16_NOSYNC  // measurement builds only: without the barrier the 16-bit fields may carry
             if (l % kSync == 0) __syncthreads();
+#endif
         }
         __syncthreads();
 #pragma unroll
@@ -486,8 +490,8 @@ __global__ void __launch_bounds__(THREADS)
     }
     for (uint32_t i = threadIdx.x; i < cwords; i += THREADS) {
         const uint32_t w = cnt16[i];
-        if (w & 0xFFFFu) atomicAdd(counts + uint32_t(rec[2 * i] & idmask), (unsigned long long)(w & 0xFFFFu));
-        if (w >> 16) atomicAdd(counts + uint32_t(rec[2 * i + 1] & idmask), (unsigned long long)(w >> 16));
+        if (w & 0xFFFFu) atomicAdd(counts + uint32_t(rec[2 * i] & idmask), CT(w & 0xFFFFu));
+        if (w >> 16) atomicAdd(counts + uint32_t(rec[2 * i + 1] & idmask), CT(w >> 16));
     }
 }
 
@@ -672,7 +676,7 @@ bool ensure_rec(saba_cu_graph* g) {
     return true;
 }
 
-template <int WPT, int T>
+template <int WPT, int T, class CT>
 bool launch_rank_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t L, uint64_t mult, void* counts,
                    cudaStream_t st) {
     const WalkVariant v = walk_variant();
@@ -687,14 +691,13 @@ bool launch_rank_t(saba_cu_graph* g, const uint64_t* keys, uint64_t nw, uint32_t
     const uint32_t ncnt = std::min<uint32_t>(g->n, v.hcnt >= 0 ? uint32_t(v.hcnt) : uint32_t(budget * 43 / 63 / 2));
     const size_t smem = sizeof(uint64_t) * nrec + sizeof(uint32_t) * ((size_t(ncnt) + 1) / 2);
     if (smem > g->smem_optin - 1024) return false;
-    auto k = walk_count_rank_kernel<WPT, T>;
+    auto k = walk_count_rank_kernel<WPT, T, CT>;
     SABA_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int occ = 0;
     SABA_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, T, smem));
     if (occ < 1) return false;
     k<<<uint32_t(g->sm_count) * occ, T, smem, st>>>(g->d_rec, g->d_rank, g->d_adj_rank, g->rec_nb, g->rec_db, nrec,
-                                                    ncnt, keys, nw, L, mult,
-                                                    static_cast<unsigned long long*>(counts));
+                                                    ncnt, keys, nw, L, mult, static_cast<CT*>(counts));
     SABA_CUDA_CHECK(cudaGetLastError());
     g->last_nrec = nrec;
     g->last_ncnt = ncnt;
@@ -827,9 +830,11 @@ void launch_walk(saba_cu_graph* g, bool c32, const uint64_t* keys, uint64_t nw, 
         return;
     }
     const bool packed = v.packed && g->d_adj_packed != nullptr;
-    if (v.rec != 0 && v.hot != 0 && v.packed && !c32 && ensure_rec(g)) {
-        const bool ok = g->hot_threads == 512 ? launch_rank_t<4, 512>(g, keys, nw, L, mult, counts, st)
-                                              : launch_rank_t<4, 1024>(g, keys, nw, L, mult, counts, st);
+    if (v.rec != 0 && v.hot != 0 && v.packed && ensure_rec(g)) {
+        using U64 = unsigned long long;
+        const bool ok = c32 ? launch_rank_t<4, 1024, uint32_t>(g, keys, nw, L, mult, counts, st)
+                        : g->hot_threads == 512 ? launch_rank_t<4, 512, U64>(g, keys, nw, L, mult, counts, st)
+                                                : launch_rank_t<4, 1024, U64>(g, keys, nw, L, mult, counts, st);
         g->last_k2 = SABA_K2_RANK;
         if (ok) return;
     }

@@ -135,13 +135,14 @@ __device__ __forceinline__ void warp_count_visit(CT* __restrict__ counts, uint32
 // barriers: every guard set before a barrier is cleared before it, so each
 // field is below 0x8000 at a barrier and below 0x8000 + 2^15 before the next
 // (kCount16Steps below bounds the steps between barriers accordingly).
+template <class CT>
 __device__ __forceinline__ void smem_count16(uint32_t* __restrict__ tab, uint32_t slot,
-                                             unsigned long long* __restrict__ counts, uint32_t vertex) {
+                                             CT* __restrict__ counts, uint32_t vertex) {
     const uint32_t sh = (slot & 1u) << 4;
     const uint32_t old = atomicAdd(tab + (slot >> 1), 1u << sh);
     if (((old >> sh) & 0xFFFFu) == 0x7FFFu) {
         atomicSub(tab + (slot >> 1), 0x8000u << sh);
-        atomicAdd(counts + vertex, 32768ull);
+        atomicAdd(counts + vertex, CT(32768));
     }
 }
 // steps between block barriers so that THREADS * WPT * steps < 2^15
