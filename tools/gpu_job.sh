@@ -1,17 +1,12 @@
-# round-2 GPU job 24: u32 global counters in the rank kernel (c32=1), cost of the 16-bit counters' barrier (nosync build: timing only)
+# round-2 GPU job 25: final build — GPU suite, smoke, ncu traffic (cfg2, cfg1), default bench and its reference arm
 set -x
 O=gpurun_out
-for w in "" "c32=1" "" "c32=1"; do
-  echo "== cfg2 [$w]" >> $O/r02x_k2.txt
-  SABA_WALK_VARIANT=$w python tools/profile_campaign.py --reps 3 2>&1 | tail -2 >> $O/r02x_k2.txt
-done
-export SABA_LIB=$PWD/paper_2410_14056_b200/_variants/nosync/libsaba_cuda.so
-echo "== cfg2 nosync build" >> $O/r02x_k2.txt
-python tools/profile_campaign.py --reps 3 2>&1 | tail -2 >> $O/r02x_k2.txt
-echo "== cfg1 nosync build" >> $O/r02x_k2.txt
-python tools/profile_campaign.py --workload cfg1 --reps 3 2>&1 | tail -2 >> $O/r02x_k2.txt
-unset SABA_LIB
-echo "== cfg1" >> $O/r02x_k2.txt
-python tools/profile_campaign.py --workload cfg1 --reps 3 2>&1 | tail -2 >> $O/r02x_k2.txt
-cat $O/r02x_k2.txt
-python -m pytest tests/test_variants_gpu.py -m gpu -x -q -p no:cacheprovider -k campaign > $O/r02x_pytest.log 2>&1; tail -3 $O/r02x_pytest.log
+python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/r02y_pytest_gpu.log 2>&1; echo "rc=$?" >> $O/r02y_pytest_gpu.log; tail -4 $O/r02y_pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/r02y_smoke.log 2>&1; tail -2 $O/r02y_smoke.log
+M=dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sectors_srcunit_tex_op_write.sum,lts__t_sectors_srcunit_tex_op_red.sum,lts__t_sectors_srcunit_tex_op_atom.sum,gpu__time_duration.sum,lts__t_requests_srcunit_tex_op_read.sum
+python tools/profile_campaign.py --reps 2 > $O/r02y_plain_cfg2.log 2>&1 && \
+ncu --metrics $M --clock-control none -k regex:walk_count -s 1 -c 1 --csv --log-file $O/r02y_ncu_k2_cfg2.csv python tools/profile_campaign.py --reps 2 > $O/r02y_ncu_cfg2.log 2>&1
+python tools/profile_campaign.py --workload cfg1 --reps 2 > $O/r02y_plain_cfg1.log 2>&1 && \
+ncu --metrics $M --clock-control none -k regex:walk_count -s 1 -c 1 --csv --log-file $O/r02y_ncu_k2_cfg1.csv python tools/profile_campaign.py --workload cfg1 --reps 2 > $O/r02y_ncu_cfg1.log 2>&1
+python bench.py --impl reference > $O/r02y_bench_reference_arm.json 2> $O/r02y_bench_reference_arm.err
+python bench.py > $O/r02y_bench_default.json 2> $O/r02y_bench_default.err; tail -c 300 $O/r02y_bench_default.json
