@@ -1,12 +1,6 @@
-# round-2 GPU job 25: final build — GPU suite, smoke, ncu traffic (cfg2, cfg1), default bench and its reference arm
+# round-2 GPU job 26: ncu --set full of the cfg3 AESC walk kernel (fat path) and the dense pull
 set -x
 O=gpurun_out
-python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/r02y_pytest_gpu.log 2>&1; echo "rc=$?" >> $O/r02y_pytest_gpu.log; tail -4 $O/r02y_pytest_gpu.log
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/r02y_smoke.log 2>&1; tail -2 $O/r02y_smoke.log
-M=dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sectors_srcunit_tex_op_write.sum,lts__t_sectors_srcunit_tex_op_red.sum,lts__t_sectors_srcunit_tex_op_atom.sum,gpu__time_duration.sum,lts__t_requests_srcunit_tex_op_read.sum
-python tools/profile_campaign.py --reps 2 > $O/r02y_plain_cfg2.log 2>&1 && \
-ncu --metrics $M --clock-control none -k regex:walk_count -s 1 -c 1 --csv --log-file $O/r02y_ncu_k2_cfg2.csv python tools/profile_campaign.py --reps 2 > $O/r02y_ncu_cfg2.log 2>&1
-python tools/profile_campaign.py --workload cfg1 --reps 2 > $O/r02y_plain_cfg1.log 2>&1 && \
-ncu --metrics $M --clock-control none -k regex:walk_count -s 1 -c 1 --csv --log-file $O/r02y_ncu_k2_cfg1.csv python tools/profile_campaign.py --workload cfg1 --reps 2 > $O/r02y_ncu_cfg1.log 2>&1
-python bench.py --impl reference > $O/r02y_bench_reference_arm.json 2> $O/r02y_bench_reference_arm.err
-python bench.py > $O/r02y_bench_default.json 2> $O/r02y_bench_default.err; tail -c 300 $O/r02y_bench_default.json
+python tools/aesc_run.py --workload cfg3 --sources 512 --reps 1 > $O/r02z_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:aesc_walk_sorted -s 2 -c 2 -o $O/r02z_aesc_walk_cfg3 python tools/aesc_run.py --workload cfg3 --sources 512 --reps 1 > $O/r02z_ncu.log 2>&1
+tail -3 $O/r02z_ncu.log
