@@ -99,6 +99,7 @@ struct AescState {
     uint32_t nheavy = 0, npieces = 0;
     DevBuf light_order;  // light rows by descending degree (dense depths)
     DevBuf recs;         // per-vertex walk records of the batch's columns (aesc_walk_rec)
+    DevBuf tile_next;    // aesc_walk_hub's tile hand-out counter
     uint32_t nlight = 0;
     bool heavy_built = false;
     cudaStream_t stream = nullptr;       // propagation (and everything else)
@@ -1047,6 +1048,118 @@ __global__ void __launch_bounds__(256, MINB)
     }
 }
 
+// K4 for long walks on L2-resident graphs, with the rho values of the
+// highest-degree vertices in shared memory. aesc_walk_sorted on such graphs
+// is bound by the SM's L1-miss request rate (one request per clock; ncu:
+// l1tex2xbar 93%): a fat gather and a rho gather per step, of which the rho
+// gathers of hubs are the cacheable half. Here a 1024-thread block takes
+// tiles of consecutive sorted walks from a device counter; consecutive walks
+// belong to one (slot, side) segment and consecutive segments to one source,
+// so a tile has one rho column almost always. The block keeps rho of that
+// column for the nhub highest-degree vertices in shared memory (reloaded
+// when the tile's column changes) and the fat record carries the neighbour's
+// hub slot in its spare high bits, so the rho of a hub is a shared-memory
+// load and only the tail (and the walks of a tile's second column, if any)
+// gathers R. Same walks, seeds and step-order sums as aesc_walk_sorted.
+template <int WPT, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+    aesc_walk_hub(const uint32_t* __restrict__ gidx, const uint32_t* __restrict__ vals, uint32_t nwalks,
+                  const WalkGroup* __restrict__ groups, const uint2* __restrict__ csr,
+                  const double* __restrict__ R, uint32_t n, uint64_t mult, const uint64_t* __restrict__ fat,
+                  uint32_t fat_idb, uint32_t fat_sh, uint32_t hub_shift,
+                  const uint32_t* __restrict__ hub_vertex, uint32_t nhub, unsigned int* __restrict__ tile_next,
+                  double* __restrict__ score) {
+    extern __shared__ double rho_s[];
+    __shared__ uint32_t s_tile, s_col;
+    constexpr uint32_t TILE = THREADS * WPT;
+    const uint32_t ntiles = (nwalks + TILE - 1) / TILE;
+    const uint64_t idmask = (uint64_t(1) << fat_idb) - 1, bmask = (uint64_t(1) << (fat_sh - fat_idb)) - 1;
+    const uint32_t dmask = (1u << (hub_shift - fat_sh)) - 1;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t cached_col = UINT32_MAX;  // block-uniform: column whose hub rho is in rho_s
+    for (;;) {
+        if (threadIdx.x == 0) {
+            s_tile = atomicAdd(tile_next, 1u);
+            if (s_tile < ntiles) s_col = groups[gidx[uint64_t(s_tile) * TILE]].col;
+        }
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= ntiles) break;
+        const uint32_t tcol = s_col;
+        if (tcol != cached_col) {
+            const double* __restrict__ Rc = R + size_t(tcol) * n;
+            for (uint32_t h = threadIdx.x; h < nhub; h += THREADS) rho_s[h] = __ldg(Rc + __ldg(hub_vertex + h));
+            cached_col = tcol;
+            __syncthreads();
+        }
+        const uint64_t base = uint64_t(tile) * TILE + uint64_t(warp) * 32 * WPT;
+        uint32_t cur[WPT], seed[WPT], len[WPT], col[WPT], hs[WPT];
+        bool mine[WPT], stepped[WPT];
+        double sc[WPT], rv[WPT];
+        uint2 rec[WPT];
+        uint32_t maxlen = 1;
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {
+            const uint64_t e = base + uint64_t(r) * 32 + lane;
+            len[r] = 1;
+            sc[r] = 0.0;
+            rv[r] = 0.0;
+            stepped[r] = false;
+            cur[r] = 0;
+            seed[r] = 0;
+            col[r] = 0;
+            hs[r] = 0;
+            mine[r] = false;
+            if (e < nwalks) {
+                const uint32_t w = vals[e];
+                const WalkGroup G = groups[gidx[e]];
+                const uint32_t local = w - G.walk_off;
+                const uint32_t side = local >= G.pairs;
+                seed[r] = walk_seed(G.edge_seed, 2 * (G.k0 + (local - side * G.pairs)) + side);
+                cur[r] = side ? G.vj : G.vi;
+                len[r] = G.len;
+                col[r] = G.col * n;  // 32-bit element offsets: kCols * n < 2^32 (checked by the host)
+                mine[r] = G.col == tcol;
+            }
+            rec[r] = len[r] > 1 ? ldg_csr(csr + cur[r]) : make_uint2(0, 1);
+            maxlen = max(maxlen, len[r]);
+        }
+        maxlen = __reduce_max_sync(0xffffffffu, maxlen);
+        for (uint32_t l = 1; l < maxlen + 2; ++l) {
+            const StepHash shs = step_hash(mult, l);
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) {
+                sc[r] += rv[r];  // step l-2 (0.0 when there was none)
+                // step l-1: cur is still x_{l-1}, hs its hub slot
+                rv[r] = 0.0;
+                if (stepped[r]) {
+                    SABA_DCHECK(hs[r] <= nhub);
+                    rv[r] = hs[r] != 0 && mine[r] ? rho_s[hs[r] - 1] : __ldg(R + (col[r] + cur[r]));
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < WPT; ++r) {
+                stepped[r] = l < len[r];
+                if (stepped[r]) {
+                    const uint32_t raw = seed[r] ^ hash_state_fast(shs, cur[r]);
+                    const uint64_t f = __ldg(reinterpret_cast<const unsigned long long*>(fat) + rec[r].x +
+                                             scaled_index(raw, rec[r].y));
+                    cur[r] = uint32_t(f & idmask);
+                    rec[r] = make_uint2(uint32_t((f >> fat_idb) & bmask), uint32_t(f >> fat_sh) & dmask);
+                    hs[r] = uint32_t(f >> hub_shift);
+                    SABA_DCHECK(cur[r] < n);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < WPT; ++r) {
+            const uint64_t e = base + uint64_t(r) * 32 + lane;
+            if (e < nwalks) score[vals[e]] = sc[r];
+        }
+        __syncthreads();  // every warp is done with s_tile / s_col / rho_s before the next tile
+    }
+}
+
 // Per-vertex walk records of one batch (beyond-L2 graphs): column c's
 // record of vertex v is {base, degree, rho_c(v)} in 16 B, so the step from
 // x_{l-1} loads ONE record that carries both what the selection needs and the
@@ -1711,6 +1824,21 @@ void set_l2_window(cudaStream_t s, const void* base, size_t bytes, const L2Windo
     SABA_CUDA_CHECK(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a));
 }
 
+// SABA_AESC_HUB=N (experiment, default off): rho of the N highest-degree
+// vertices in shared memory for long walks on the fat path (aesc_walk_hub).
+// Measured on cfg3 (profiles/r02_aesc_hub_rho_experiment.txt): the walk
+// kernels get ~7% faster with two workers, but a 1024-thread block with a
+// 96 KB table leaves the other worker's propagation kernels less of each SM
+// (propagation +20%), and with one worker nothing changes: the rho gathers of
+// hubs were L1 hits already. 9.21 s without, 9.27-9.48 s with.
+uint32_t aesc_hub_count() {
+    static const uint32_t v = [] {
+        const char* e = getenv("SABA_AESC_HUB");
+        return e ? uint32_t(atoi(e)) : 0u;
+    }();
+    return v;
+}
+
 void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb, const double* R,
                const uint32_t* bits, uint64_t mult, double* g_hat_dev, uint32_t* launches,
                const uint4* recs = nullptr, float* walk_kernel_ms = nullptr) {
@@ -1761,7 +1889,19 @@ void run_tiles(saba_cu_graph* g, AescState* st, cudaStream_t s, TileBuilder& tb,
             }
         }
         if (walk_kernel_ms) SABA_CUDA_CHECK(cudaEventRecord(st->ev_walk[0], s));
-        if (short_walks)
+        const bool hub = fat && !short_walks && !recs && !bits && g->d_adj_fat_hub != nullptr;
+        if (hub) {
+            constexpr int T = 1024, WPT = 4;
+            auto k = aesc_walk_hub<WPT, T>;
+            const size_t smem = sizeof(double) * g->fat_hub_count;
+            SABA_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            auto* ctr = static_cast<unsigned int*>(st->tile_next.ensure(sizeof(unsigned int), s));
+            SABA_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
+            const uint32_t ntiles = (nw + T * WPT - 1) / (T * WPT);
+            k<<<std::min<uint32_t>(ntiles, uint32_t(g->sm_count)), T, smem, s>>>(
+                out_g, out_w, nw, dg, g->d_csr, R, g->n, mult, g->d_adj_fat_hub, g->fat_idb, g->fat_sh,
+                g->fat_hub_shift, g->d_fat_hub_vertex, g->fat_hub_count, ctr, score);
+        } else if (short_walks)
             walk_dispatch<kShortWpt, kShortMinb>(L, fat, packed, f16);
         else
             walk_dispatch<4, 5>(L, fat, packed, false);
@@ -2024,8 +2164,10 @@ void aesc_run(saba_cu_graph* g, const saba_cu_aesc_config& cfg, const uint32_t* 
         saba_cu_graph* rg = out.reps[r];
         if (r) locks.emplace_back(rg->mu);  // replica 0 is g (held by the caller)
         DeviceScope scope(rg->device);
-        if (fat_fits_l2(rg) && aesc_fat_enabled())
+        if (fat_fits_l2(rg) && aesc_fat_enabled()) {
             ensure_fat(rg);  // before the workers start
+            if (aesc_hub_count() && plan.max_tau >= kShortWalk) ensure_fat_hub(rg, aesc_hub_count());
+        }
         else if (plan.max_tau < kShortWalk && aesc_fat16_enabled())
             ensure_fat16(rg);
         for (int w = 0; w < nworkers; ++w) {

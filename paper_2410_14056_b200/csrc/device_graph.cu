@@ -1,10 +1,12 @@
 // K0: device CSR upload and the handle lifecycle; library identification.
+#include <algorithm>
 #include <chrono>
 #include <mutex>
 #include <omp.h>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "device_graph.cuh"
 #include "saba_hash.cuh"
@@ -73,6 +75,53 @@ bool ensure_fat16(saba_cu_graph* g) {
     build_fat16_kernel<<<g->sm_count * 8, 256>>>(g->d_csr, g->d_adj, 2 * g->m, g->d_adj_fat16);
     SABA_CUDA_CHECK(cudaGetLastError());
     SABA_CUDA_CHECK(cudaDeviceSynchronize());
+    return true;
+}
+
+// Fat adjacency + hub slot: slot s -> fat[s] | (hub slot of adj[s] + 1) << shift
+// (0 = not a hub). Hubs are the highest-degree vertices, ties by ascending id;
+// the order is computed on the host (the fat form exists only for small,
+// L2-resident graphs).
+namespace {
+__global__ void build_fat_hub_kernel(const uint64_t* __restrict__ fat, const uint32_t* __restrict__ adj,
+                                     const uint32_t* __restrict__ slot_of, uint64_t two_m, uint32_t shift,
+                                     uint64_t* __restrict__ out) {
+    for (uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < two_m;
+         s += uint64_t(gridDim.x) * blockDim.x)
+        out[s] = fat[s] | (uint64_t(slot_of[adj[s]]) << shift);
+}
+}  // namespace
+
+bool ensure_fat_hub(saba_cu_graph* g, uint32_t max_hubs) {
+    if (g->fat_hub_tried) return g->d_adj_fat_hub != nullptr;
+    g->fat_hub_tried = true;
+    if (!ensure_fat(g) || max_hubs == 0) return false;
+    uint32_t db = 1;
+    while (db < 32 && (g->max_degree >> db) != 0) ++db;
+    const uint32_t shift = g->fat_sh + db;
+    if (shift + 8 > 64) return false;  // fewer than 255 hubs are not worth a table
+    const uint32_t spare = 64 - shift;
+    const uint32_t h = uint32_t(std::min<uint64_t>({uint64_t(g->n), (spare >= 32 ? UINT32_MAX : (1u << spare) - 1u),
+                                                    uint64_t(max_hubs)}));
+    const uint32_t n = g->n;
+    std::vector<uint32_t> order(n), slot_of(n, 0u);
+    for (uint32_t v = 0; v < n; ++v) order[v] = v;
+    const auto& off = g->h_off;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+        return off[a + 1] - off[a] > off[b + 1] - off[b];
+    });
+    for (uint32_t i = 0; i < h; ++i) slot_of[order[i]] = i + 1;
+    DevBuf d_slot;
+    uint32_t* ds = static_cast<uint32_t*>(d_slot.ensure(sizeof(uint32_t) * n));
+    g->d_fat_hub_vertex = static_cast<uint32_t*>(pool_alloc(sizeof(uint32_t) * h));
+    g->d_adj_fat_hub = static_cast<uint64_t*>(pool_alloc(sizeof(uint64_t) * 2 * g->m));
+    SABA_CUDA_CHECK(cudaMemcpy(ds, slot_of.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+    SABA_CUDA_CHECK(cudaMemcpy(g->d_fat_hub_vertex, order.data(), sizeof(uint32_t) * h, cudaMemcpyHostToDevice));
+    build_fat_hub_kernel<<<g->sm_count * 8, 256>>>(g->d_adj_fat, g->d_adj, ds, 2 * g->m, shift, g->d_adj_fat_hub);
+    SABA_CUDA_CHECK(cudaGetLastError());
+    SABA_CUDA_CHECK(cudaDeviceSynchronize());
+    g->fat_hub_count = h;
+    g->fat_hub_shift = shift;
     return true;
 }
 
@@ -320,6 +369,8 @@ saba_cu_graph::~saba_cu_graph() {
     if (d_adj_packed) saba_cu::pool_free(d_adj_packed);
     if (d_adj_fat) saba_cu::pool_free(d_adj_fat);
     if (d_adj_fat16) saba_cu::pool_free(d_adj_fat16);
+    if (d_adj_fat_hub) saba_cu::pool_free(d_adj_fat_hub);
+    if (d_fat_hub_vertex) saba_cu::pool_free(d_fat_hub_vertex);
     if (d_csr_hot) saba_cu::pool_free(d_csr_hot);
     if (d_hot_vertex) saba_cu::pool_free(d_hot_vertex);
     if (d_rec) saba_cu::pool_free(d_rec);

@@ -118,6 +118,13 @@ struct saba_cu_graph {
     bool fat16_tried = false;
     uint32_t fat_idb = 0, fat_sh = 0;
     bool fat_tried = false;
+    // fat adjacency with a hub slot in its spare high bits (AESC long walks on
+    // L2-resident graphs): the rho values of the highest-degree vertices of
+    // the column a block is walking live in shared memory, indexed by slot-1
+    uint64_t* d_adj_fat_hub = nullptr;
+    uint32_t* d_fat_hub_vertex = nullptr;  // slot -> vertex
+    uint32_t fat_hub_count = 0, fat_hub_shift = 0;
+    bool fat_hub_tried = false;
     // Hub-privatised counting: {base, degree | (hot slot + 1) << hot_shift};
     // the top-degree vertices count their visits in shared memory.
     uint2* d_csr_hot = nullptr;
@@ -171,6 +178,8 @@ const IdVec& host_adj(saba_cu_graph* g);  // D2H once, then cached
 // Build the fat adjacency once (false if {id, base, degree} exceed 64 bits).
 bool ensure_fat(saba_cu_graph* g);
 bool ensure_fat16(saba_cu_graph* g);
+bool ensure_fat_hub(saba_cu_graph* g, uint32_t max_hubs);
+bool ensure_fat_hub(saba_cu_graph* g, uint32_t max_hubs);
 // Fat adjacency is worth it while it stays comfortably L2-resident.
 inline bool fat_fits_l2(const saba_cu_graph* g) { return 16 * g->m <= (uint64_t(48) << 20); }
 constexpr uint32_t kPackBits = 21;

@@ -49,6 +49,8 @@ AESC_ENV = [{}, {"SABA_AESC_FAT": "0"}, {"SABA_AESC_FAT16": "0"}, {"SABA_AESC_BI
             {"SABA_SHORT_STEPS": "0"}, {"SABA_SHORT_STEPS": "1000"},
             {"SABA_AESC_REC": "2"}, {"SABA_AESC_REC": "2", "SABA_SHORT_STEPS": "0"},
             {"SABA_PULL_SKIP": "0"}, {"SABA_PULL_SKIP": "1"}, {"SABA_PULL_SKIP": "1", "SABA_PULL_STATIC": "1"},
+            {"SABA_AESC_HUB": "0"}, {"SABA_AESC_HUB": "300"}, {"SABA_AESC_HUB": "300", "SABA_AESC_WORKERS": "1"},
+            {"SABA_AESC_HUB": "16000", "SABA_SHORT_STEPS": "0"},
             {"SABA_AESC_FAT": "0", "SABA_AESC_FAT16": "0", "SABA_AESC_REC": "0"},
             {"SABA_AESC_FAT": "0", "SABA_AESC_FAT16": "0", "SABA_AESC_REC": "0", "SABA_AESC_BITMAP": "1"}]
 
