@@ -1,13 +1,10 @@
-# round-2 GPU job 29: aesc_walk_hub (hub rho in shared memory, tile hand-out) — parity and cfg3 timing by hub count
+# round-2 GPU job 30: final build — GPU suite, ncu traffic (cfg2, cfg1), default bench
 set -x
 O=gpurun_out
-python -m pytest tests/test_aesc_gpu.py tests/test_variants_gpu.py tests/test_fullsize_reference_gpu.py -m gpu -x -q -p no:cacheprovider -k "aesc or cfg3" > $O/r02ac_pytest.log 2>&1; echo "rc=$?" >> $O/r02ac_pytest.log; tail -4 $O/r02ac_pytest.log
-for h in 0 12288 4096 8192 16383 0 12288; do
-  echo "== cfg3 HUB=$h" >> $O/r02ac_hub.txt
-  SABA_AESC_HUB=$h python tools/aesc_run.py --workload cfg3 --reps 2 2>/dev/null | grep "aesc:" >> $O/r02ac_hub.txt
-done
-for h in 0 12288; do
-  echo "== cfg3 HUB=$h workers=1" >> $O/r02ac_hub.txt
-  SABA_AESC_WORKERS=1 SABA_AESC_HUB=$h python tools/aesc_run.py --workload cfg3 --reps 2 2>/dev/null | grep "aesc:" >> $O/r02ac_hub.txt
-done
-cat $O/r02ac_hub.txt
+python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/r02ad_pytest_gpu.log 2>&1; echo "rc=$?" >> $O/r02ad_pytest_gpu.log; tail -4 $O/r02ad_pytest_gpu.log
+M=dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sectors_srcunit_tex_op_write.sum,lts__t_sectors_srcunit_tex_op_red.sum,lts__t_sectors_srcunit_tex_op_atom.sum,gpu__time_duration.sum,lts__t_requests_srcunit_tex_op_read.sum
+python tools/profile_campaign.py --reps 2 > $O/r02ad_plain_cfg2.log 2>&1 && \
+ncu --metrics $M --clock-control none -k regex:walk_count -s 1 -c 1 --csv --log-file $O/r02ad_ncu_k2_cfg2.csv python tools/profile_campaign.py --reps 2 > $O/r02ad_ncu_cfg2.log 2>&1
+python tools/profile_campaign.py --workload cfg1 --reps 2 > $O/r02ad_plain_cfg1.log 2>&1 && \
+ncu --metrics $M --clock-control none -k regex:walk_count -s 1 -c 1 --csv --log-file $O/r02ad_ncu_k2_cfg1.csv python tools/profile_campaign.py --workload cfg1 --reps 2 > $O/r02ad_ncu_cfg1.log 2>&1
+python bench.py > $O/r02ad_bench_default.json 2> $O/r02ad_bench_default.err; tail -c 300 $O/r02ad_bench_default.json
