@@ -53,6 +53,11 @@ SABA_API const char* saba_cu_last_error(void);
 SABA_API const char* saba_cu_version(void);
 /* number of CUDA devices visible (0 on a CPU-only host) */
 SABA_API int saba_cu_device_count(void);
+/* Page-locked host memory for result buffers (counts, g_hat): copies into such
+ * a buffer are direct DMA instead of a staged copy. No reference counterpart
+ * (the reference has no device); free with saba_cu_pinned_free. */
+SABA_API int saba_cu_pinned_alloc(uint64_t bytes, void** out);
+SABA_API int saba_cu_pinned_free(void* p);
 
 /* ======================================================================
  * Host graphs (graph.hpp:28-247, gen.hpp; BASELINE generators)

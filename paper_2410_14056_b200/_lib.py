@@ -66,6 +66,8 @@ SIGNATURES = {
     "saba_cu_last_error": (C.c_char_p, []),
     "saba_cu_version": (C.c_char_p, []),
     "saba_cu_device_count": (C.c_int, []),
+    "saba_cu_pinned_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
+    "saba_cu_pinned_free": (C.c_int, [C.c_void_p]),
     "saba_hgraph_from_edges": (C.c_int, [C.c_uint32, u32p, C.c_uint64, vpp]),
     "saba_hgraph_from_csr": (C.c_int, [C.c_uint32, u32p, u32p, vpp]),
     "saba_gen_erdos_renyi": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, vpp]),

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -248,6 +249,38 @@ def _report(r: L.CampaignReportC) -> CampaignReport:
                           r.launches, r.shard_walks, K2_KERNELS.get(r.kernel, str(r.kernel)))
 
 
+class _PinnedCounts:
+    """A page-locked uint64[n] landing buffer (saba_cu_pinned_alloc): the
+    campaign's counts arrive by direct DMA instead of a staged copy."""
+
+    def __init__(self, n: int):
+        self.n = n
+        p = C.c_void_p()
+        L.check(L.lib().saba_cu_pinned_alloc(8 * max(n, 1), C.byref(p)), "pinned_alloc")
+        self._p = p
+        self.array = np.frombuffer((C.c_uint64 * max(n, 1)).from_address(p.value), dtype=np.uint64)[:n]
+
+    def __del__(self):
+        try:
+            self.array = None
+            L.lib().saba_cu_pinned_free(self._p)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+_scratch = threading.local()
+
+
+def _scratch_counts(n: int) -> np.ndarray:
+    """Per-thread landing buffer for a campaign's counts, page-locked and
+    reused from call to call (every entry is rewritten by each call)."""
+    buf = getattr(_scratch, "buf", None)
+    if buf is None or buf.n != n:
+        buf = _PinnedCounts(n)
+        _scratch.buf = buf
+    return buf.array
+
+
 def run_walk_campaign(g: Graph, cfg: CampaignConfig, sink: VisitCountSink, *,
                       total_walks: int = 0, shard_index: int = 0, shard_count: int = 1,
                       device: int = 0, devices=None) -> CampaignReport:
@@ -264,13 +297,13 @@ def run_walk_campaign(g: Graph, cfg: CampaignConfig, sink: VisitCountSink, *,
         raise TypeError("the GPU campaign supports VisitCountSink only")
     if len(sink.counts) != g.n:
         raise ValueError("sink size != vertex count")
-    counts = np.zeros(g.n, np.uint64)
+    counts = _scratch_counts(g.n)  # every entry is written by the call
     rep = L.CampaignReportC()
     c = _cfg_c(cfg, total_walks, shard_index, shard_count)
     h = g.device_group(devices) if devices is not None else g.device_handle(device)
     L.check(L.lib().saba_cu_walk_campaign(h, C.byref(c), L.ptr(counts, L.u64p), C.byref(rep)),
             "walk_campaign")
-    sink.counts += counts
+    np.add(sink.counts, counts, out=sink.counts)  # VisitCountSink::absorb (walker.hpp:360-364)
     out = _report(rep)
     # the reference collects stats in lane modes with L > 1 (walker.hpp:471)
     if cfg.collect_stats and cfg.length > 1:
