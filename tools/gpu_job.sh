@@ -1,8 +1,4 @@
-# round-2 GPU job 34: short-walk shape threshold on the L2-resident cfg3 (the short shape is issue-bound there)
+# round-2 GPU job 35: randomised campaign parity sweep (every K2 variant x 200 seeded cases vs the CPU oracle)
 set -x
 O=gpurun_out
-for t in 20 0 8 12 20 0; do
-  echo "== cfg3 SABA_SHORT_STEPS=$t" >> $O/r02ah_short.txt
-  SABA_SHORT_STEPS=$t python tools/aesc_run.py --workload cfg3 --reps 2 2>/dev/null | grep "aesc:" >> $O/r02ah_short.txt
-done
-cat $O/r02ah_short.txt
+python tools/fuzz_campaign.py --cases 200 > $O/r02ai_fuzz_campaign.log 2>&1; echo "rc=$?" >> $O/r02ai_fuzz_campaign.log; tail -16 $O/r02ai_fuzz_campaign.log
