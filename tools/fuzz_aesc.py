@@ -74,15 +74,21 @@ def worker(n_cases, use_oracle, out_path):
     res = {}
     O = None
     if use_oracle:
-        from oracle.oracle import Oracle  # checker only
+        from oracle.oracle import Oracle, Reference  # checkers only
         O = Oracle()
+        R = Reference() if use_oracle == "ref" else None
     for c in cases(n_cases):
         g = make_graph(sb, c)
         src = sources_of(c, g.n)
         if use_oracle:
             try:
-                r = O.aesc(g.offsets, g.adjacency, epsilon=c["eps"], delta=c["delta"], master_seed=c["seed"],
-                           per_edge_tau=c["per_edge"], switch_depth_cap=c["cap"], sources=src)
+                if R is not None:  # the reference headers compiled in place (oracle/_ref)
+                    r = R.aesc(R.from_csr(g.offsets, g.adjacency), epsilon=c["eps"], delta=c["delta"],
+                               master_seed=c["seed"], per_edge_tau=c["per_edge"], switch_depth_cap=c["cap"],
+                               sources=src)
+                else:
+                    r = O.aesc(g.offsets, g.adjacency, epsilon=c["eps"], delta=c["delta"], master_seed=c["seed"],
+                               per_edge_tau=c["per_edge"], switch_depth_cap=c["cap"], sources=src)
             except (ValueError, RuntimeError) as e:  # e.g. a walk budget beyond 2^63 (aesc.hpp:117-126)
                 res[f"e{c['id']}"] = np.array([1 if isinstance(e, ValueError) else 2])
                 continue
@@ -111,11 +117,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--worker", action="store_true")
     ap.add_argument("--oracle", action="store_true")
+    ap.add_argument("--checker", default="oracle", choices=["oracle", "ref"],
+                    help="oracle = the C restatement, ref = the compiled reference (oracle/_ref)")
     ap.add_argument("--cases", type=int, default=30)
     ap.add_argument("--out", default="/tmp/fuzz_aesc.npz")
     a = ap.parse_args()
     if a.worker:
-        worker(a.cases, a.oracle, a.out)
+        worker(a.cases, a.checker if a.oracle else "", a.out)
         return
 
     def run(env_extra, extra, tag):
@@ -129,7 +137,7 @@ def main():
             raise SystemExit(1)
         return dict(np.load(out))
 
-    want = run({}, ["--oracle"], "oracle")
+    want = run({}, ["--oracle", "--checker", a.checker], "oracle")
     cs = cases(a.cases)
     bad = 0
     for i, envx in enumerate(ENVS):
@@ -159,10 +167,11 @@ def main():
             if not ok:
                 bad += 1
                 print(f"MISMATCH env {envx} case {c}")
-        print(f"env {envx}: {len(cs)} cases within 1e-9 of the oracle (counts and tau~ equal); worst rel {worst:.2e} over |ref| > 1e-12")
+        print(f"env {envx}: {len(cs)} cases within 1e-9 of the checker (counts and tau~ equal); worst rel {worst:.2e} over |ref| > 1e-12")
     nerr = sum(1 for k in want if k.startswith("e"))
     print("fuzz aesc:", "FAILED" if bad else "ok", f"({len(ENVS)} switch sets x {len(cs)} cases, {nerr} of them "
-          "rejected alike by the oracle and the GPU path)")
+          f"rejected alike by the checker and the GPU path; checker: "
+          f"{'the compiled reference' if a.checker == 'ref' else 'the C oracle'})")
     raise SystemExit(1 if bad else 0)
 
 

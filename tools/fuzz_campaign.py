@@ -80,12 +80,19 @@ def worker(n_cases, use_oracle):
     res = {}
     O = None
     if use_oracle:
-        from oracle.oracle import Oracle  # checker only
+        from oracle.oracle import Oracle, Reference  # checkers only
         O = Oracle()
+        R = Reference() if use_oracle == "ref" else None
     for c in cases(n_cases):
         g = make_graph(sb, c)
         if use_oracle:
-            if "K" in c:
+            if R is not None:  # the reference headers compiled in place (oracle/_ref)
+                rg = R.from_csr(g.offsets, g.adjacency)
+                if "K" in c:
+                    want = R.campaign(rg, c["K"], c["L"], master=c["seed"])[0]
+                else:
+                    want = R.campaign_kv(rg, c["L"], W=c["W"], master=c["seed"])[0]
+            elif "K" in c:
                 want = O.campaign_counts(g.offsets, g.adjacency, K=c["K"], length=c["L"], master=c["seed"])
             else:
                 kv = O.uniform_start_counts(g.n, c["W"], c["seed"])
@@ -111,10 +118,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--worker", action="store_true")
     ap.add_argument("--oracle", action="store_true")
+    ap.add_argument("--checker", default="oracle", choices=["oracle", "ref"],
+                    help="oracle = the C restatement, ref = the compiled reference (oracle/_ref)")
     ap.add_argument("--cases", type=int, default=40)
     a = ap.parse_args()
     if a.worker:
-        worker(a.cases, a.oracle)
+        worker(a.cases, a.checker if a.oracle else "")
         return
 
     def run(env_extra, extra):
@@ -129,7 +138,7 @@ def main():
         line = [x for x in r.stdout.splitlines() if x.startswith("FUZZ_JSON ")][-1]
         return json.loads(line[len("FUZZ_JSON "):])
 
-    want = run({}, ["--oracle"])
+    want = run({}, ["--oracle", "--checker", a.checker])
     bad = 0
     for v in VARIANTS:
         got = run({"SABA_WALK_VARIANT": v} if v else {}, [])
@@ -139,8 +148,9 @@ def main():
             if got[k]["digest"] != w["digest"]:
                 bad += 1
                 print(f"MISMATCH variant [{v}] case {k}: {cases(a.cases)[int(k)]}")
-        print(f"variant [{v}]: {len(want)} cases equal to the oracle; kernels {kernels}")
-    print("fuzz campaign:", "FAILED" if bad else "ok", f"({len(VARIANTS)} variants x {len(want)} cases)")
+        print(f"variant [{v}]: {len(want)} cases equal to the checker; kernels {kernels}")
+    print("fuzz campaign:", "FAILED" if bad else "ok", f"({len(VARIANTS)} variants x {len(want)} cases, checker: "
+          f"{'the compiled reference' if a.checker == 'ref' else 'the C oracle'})")
     raise SystemExit(1 if bad else 0)
 
 
