@@ -1,5 +1,8 @@
-# round-2 GPU job 37: randomised parity sweeps with the compiled reference (oracle/_ref) as the checker
+# round-2 GPU job 38: propagation depths per CUDA-graph replay on cfg3 (default 8)
 set -x
 O=gpurun_out
-python tools/fuzz_campaign.py --cases 200 --checker ref > $O/r02ak_fuzz_campaign_ref.log 2>&1; echo "rc=$?" >> $O/r02ak_fuzz_campaign_ref.log; tail -4 $O/r02ak_fuzz_campaign_ref.log
-python tools/fuzz_aesc.py --cases 100 --checker ref > $O/r02ak_fuzz_aesc_ref.log 2>&1; echo "rc=$?" >> $O/r02ak_fuzz_aesc_ref.log; tail -4 $O/r02ak_fuzz_aesc_ref.log
+for d in 8 16 32 8 16; do
+  echo "== cfg3 SABA_DEPTHS_PER_GRAPH=$d" >> $O/r02al_depths.txt
+  SABA_DEPTHS_PER_GRAPH=$d python tools/aesc_run.py --workload cfg3 --reps 2 2>/dev/null | grep "aesc:" >> $O/r02al_depths.txt
+done
+cat $O/r02al_depths.txt
