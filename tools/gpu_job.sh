@@ -1,8 +1,4 @@
-# round-2 GPU job 38: propagation depths per CUDA-graph replay on cfg3 (default 8)
+# round-2 GPU job 39: full-size multi-replica check on one GPU (cfg2 x 2/8 logical replicas, cfg3 AESC x 2)
 set -x
 O=gpurun_out
-for d in 8 16 32 8 16; do
-  echo "== cfg3 SABA_DEPTHS_PER_GRAPH=$d" >> $O/r02al_depths.txt
-  SABA_DEPTHS_PER_GRAPH=$d python tools/aesc_run.py --workload cfg3 --reps 2 2>/dev/null | grep "aesc:" >> $O/r02al_depths.txt
-done
-cat $O/r02al_depths.txt
+python tools/multi_replica_fullsize.py > $O/r02am_multi_replica.log 2>&1; echo "rc=$?" >> $O/r02am_multi_replica.log; tail -8 $O/r02am_multi_replica.log
