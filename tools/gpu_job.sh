@@ -1,4 +1,6 @@
-# round-2 GPU job 39: full-size multi-replica check on one GPU (cfg2 x 2/8 logical replicas, cfg3 AESC x 2)
+# round-2 GPU job 40: ncu --set full of K2 on cfg1 (walk_count_fat_priv_kernel)
 set -x
 O=gpurun_out
-python tools/multi_replica_fullsize.py > $O/r02am_multi_replica.log 2>&1; echo "rc=$?" >> $O/r02am_multi_replica.log; tail -8 $O/r02am_multi_replica.log
+python tools/profile_campaign.py --workload cfg1 --reps 2 > $O/r02an_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:walk_count -s 1 -c 1 -o $O/r02an_k2_cfg1 python tools/profile_campaign.py --workload cfg1 --reps 2 > $O/r02an_ncu.log 2>&1
+tail -2 $O/r02an_ncu.log
