@@ -4,8 +4,8 @@ switch-depth cap, source subset or the whole graph — under a few library
 switches (one process each) against the CPU oracle: tau~ and pair / step
 counts equal, g_hat (and s_hat for whole-graph runs) within 1e-9 relative.
 
-  python tools/fuzz_aesc.py              # driver
-  python tools/fuzz_aesc.py --worker     # one switch set (from the environment)
+  python tests/qa/fuzz_aesc.py              # driver
+  python tests/qa/fuzz_aesc.py --worker     # one switch set (from the environment)
 """
 import argparse
 import json
@@ -15,7 +15,7 @@ import sys
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 RTOL, ATOL = 1e-9, 1e-15

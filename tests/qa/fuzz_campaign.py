@@ -4,8 +4,8 @@ mode, shard count — is run by every K2 variant (one process per variant: the
 library reads SABA_WALK_VARIANT once) and every variant's counts must equal
 the CPU oracle's, bit for bit.
 
-  python tools/fuzz_campaign.py            # driver: spawns the variants, compares, prints a summary
-  python tools/fuzz_campaign.py --worker   # one variant (env SABA_WALK_VARIANT), JSON of count digests
+  python tests/qa/fuzz_campaign.py            # driver: spawns the variants, compares, prints a summary
+  python tests/qa/fuzz_campaign.py --worker   # one variant (env SABA_WALK_VARIANT), JSON of count digests
 """
 import argparse
 import hashlib
@@ -16,7 +16,7 @@ import sys
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 VARIANTS = ["", "rec=0", "fat=0", "fat=0,rec=0", "fat=0,rec=0,hot=0", "priv=0", "fat=0,hrec=7,hcnt=13",

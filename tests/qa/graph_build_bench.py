@@ -3,14 +3,14 @@ generators on the device (csrc/graph_build.cu) vs the host builders and the
 reference's own Graph::from_edges (oracle/_ref, std::sort, graph.hpp:86-105).
 Every device result is checked equal to the host result before it is timed.
 
-    python tools/graph_build_bench.py > profiles/r01_graph_build.txt
+    python tests/qa/graph_build_bench.py > profiles/r01_graph_build.txt
 """
 import json
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 
 import paper_2410_14056_b200 as sb  # noqa: E402

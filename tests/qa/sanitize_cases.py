@@ -4,10 +4,10 @@ dynamic work list of the AESC propagation, the warp-aggregated frontier
 appends, the walk kernels' shared-memory hub counters, the device graph
 builder's lock-free union-find, and the multi-replica combine.
 
-  compute-sanitizer --tool memcheck  python tools/sanitize_cases.py
-  compute-sanitizer --tool racecheck python tools/sanitize_cases.py
-  compute-sanitizer --tool synccheck python tools/sanitize_cases.py
-  compute-sanitizer --tool initcheck python tools/sanitize_cases.py
+  compute-sanitizer --tool memcheck  python tests/qa/sanitize_cases.py
+  compute-sanitizer --tool racecheck python tests/qa/sanitize_cases.py
+  compute-sanitizer --tool synccheck python tests/qa/sanitize_cases.py
+  compute-sanitizer --tool initcheck python tests/qa/sanitize_cases.py
 
 Every result is also checked against the CPU oracle, so a run that the
 sanitizer slows down or perturbs still has to be exact.
@@ -17,7 +17,7 @@ import sys
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import paper_2410_14056_b200 as sb  # noqa: E402

@@ -13,7 +13,6 @@ import paper_2410_14056_b200 as sb  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="cfg3")
 ap.add_argument("--sources", type=int, default=0, help="0 = all")
-ap.add_argument("--oracle-check", type=int, default=0, help="check this many sources vs oracle")
 ap.add_argument("--reps", type=int, default=2, help="timed runs; the last one is reported")
 a = ap.parse_args()
 t = time.time()
@@ -41,17 +40,6 @@ print(f"aesc: wall {wall:.2f}s est.seconds {est.seconds:.2f}s plan {est.plan_sec
       f"pairs {est.total_walk_pairs:.3e} steps {est.total_walk_steps:.3e} "
       f"-> {est.total_walk_steps/max(est.walk_ms*1e-3,1e-9):.3e} walk steps/s launches {est.launches}",
       flush=True)
-if a.oracle_check:
-    from oracle.oracle import Oracle
-    O = Oracle()
-    chk = (src if src is not None else np.arange(g.n, dtype=np.uint32))[: a.oracle_check]
-    t = time.time()
-    ref = O.aesc(g.offsets, g.adjacency, epsilon=eps, delta=delta, sources=chk)
-    sub = sb.aesc(g, cfg, sources=chk)
-    ok_tt = np.array_equal(sub.plan.tau_tilde[chk], ref.tau_tilde[chk])
-    rel = np.abs(sub.g_hat - ref.g_hat) / (np.abs(ref.g_hat) + 1e-300)
-    print(f"oracle check {len(chk)} sources ({time.time()-t:.1f}s): tau~ equal {ok_tt} "
-          f"max rel {rel.max():.3e} pairs {sub.total_walk_pairs}=={ref.total_walk_pairs}", flush=True)
 import json  # noqa: E402
 print("AESC_JSON " + json.dumps({"workload": a.workload, "sources": int(a.sources), "walk_steps": est.total_walk_steps,
                                  "walk_pairs": est.total_walk_pairs, "edge_visits": est.edge_visits,
