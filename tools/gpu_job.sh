@@ -1,12 +1,6 @@
-# round-2 GPU job 43: final default bench line and its reference arm (all traffic JSONs stamped with this build); AESC launch lists
+# round-2 GPU job 44: bench.py --gpus 2 --dist-backend gloo under torch.distributed.run (two ranks sharing the GPU), final build
 set -x
 O=gpurun_out
-python bench.py > $O/r02aq_bench_default.json 2> $O/r02aq_bench_default.err; tail -c 300 $O/r02aq_bench_default.json
-python bench.py --impl reference > $O/r02aq_bench_reference_arm.json 2> $O/r02aq_bench_reference_arm.err
-python tools/aesc_run.py --workload cfg3 --sources 2048 --reps 1 > $O/r02aq_plain3.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/r02aq_launches_aesc_cfg3.csv python tools/aesc_run.py --workload cfg3 --sources 2048 --reps 1 > $O/r02aq_ncu3.log 2>&1
-python tools/launch_summary.py $O/r02aq_launches_aesc_cfg3.csv > $O/r02aq_launches_aesc_cfg3_summary.txt
-python tools/aesc_run.py --workload cfg5 --sources 256 --reps 1 > $O/r02aq_plain5.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/r02aq_launches_aesc_cfg5.csv python tools/aesc_run.py --workload cfg5 --sources 256 --reps 1 > $O/r02aq_ncu5.log 2>&1
-python tools/launch_summary.py $O/r02aq_launches_aesc_cfg5.csv > $O/r02aq_launches_aesc_cfg5_summary.txt
-head -8 $O/r02aq_launches_aesc_cfg3_summary.txt; head -6 $O/r02aq_launches_aesc_cfg5_summary.txt
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --dist-backend gloo --workload cfg1 --steps 5 --warmup 3 > $O/r02ar_bench_gloo2_cfg1.json 2> $O/r02ar_gloo2_cfg1.err; tail -c 600 $O/r02ar_bench_gloo2_cfg1.json
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --dist-backend gloo --workload cfg3 > $O/r02ar_bench_gloo2_cfg3.json 2> $O/r02ar_gloo2_cfg3.err; tail -c 600 $O/r02ar_bench_gloo2_cfg3.json
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 2 --dist-backend gloo --steps 5 --warmup 3 --no-aesc > $O/r02ar_bench_gloo2_cfg2.json 2> $O/r02ar_gloo2_cfg2.err; tail -c 600 $O/r02ar_bench_gloo2_cfg2.json
