@@ -374,6 +374,10 @@ def walk_roofline(args, kern_ms, steps_per_rank, ms_per_step, kernel):
             "model": "achieved = steps x 64 B (one 32 B sector for {base,deg} + one for the neighbour id, "
                      "SURVEY §8d) / K2 launch time (CUDA events on the launch stream)"}
     roof["kernel"] = "K2 " + K2_DESCR.get(kernel, kernel)
+    if roof["frac"] > 1.0:
+        roof["note"] = ("frac > 1: the 64 B/step model charges every step two DRAM sectors, while the records and "
+                        "counters of the highest-degree vertices are served from shared memory and part of the "
+                        "neighbour sectors hit in L2; `traffic` is the DRAM bytes ncu measured per launch")
     if args.workload == "cfg1":
         # the cfg1 CSR (4.5 MB) is L2-resident: HBM is not the bound, L2
         # random-sector throughput is (SURVEY §8d asks for it beside HBM)
