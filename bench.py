@@ -374,7 +374,11 @@ def walk_roofline(args, kern_ms, steps_per_rank, ms_per_step, kernel):
             "model": "achieved = steps x 64 B (one 32 B sector for {base,deg} + one for the neighbour id, "
                      "SURVEY §8d) / K2 launch time (CUDA events on the launch stream)"}
     roof["kernel"] = "K2 " + K2_DESCR.get(kernel, kernel)
-    if roof["frac"] > 1.0:
+    if roof["frac"] > 1.0 and "fat" in kernel:
+        roof["note"] = ("frac > 1: the 64 B/step model charges every step two DRAM sectors, while this kernel takes "
+                        "one gather per step from an L2-resident array and counts in shared memory; HBM is not the "
+                        "bound, see `l2`")
+    elif roof["frac"] > 1.0:
         roof["note"] = ("frac > 1: the 64 B/step model charges every step two DRAM sectors, while the records and "
                         "counters of the highest-degree vertices are served from shared memory and part of the "
                         "neighbour sectors hit in L2; `traffic` is the DRAM bytes ncu measured per launch")
