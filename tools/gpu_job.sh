@@ -1,7 +1,6 @@
-# round-2 GPU job 45: bench.py smoke after the roofline note (cfg2 without the AESC block, cfg1)
+# round-2 GPU job 46: committed bench lines regenerated with the final bench.py (default with the AESC block, cfg1)
 set -x
 O=gpurun_out
-python bench.py --no-aesc --steps 5 > $O/r02as_bench_cfg2.json 2> $O/r02as_bench_cfg2.err; echo "rc=$?"; python -c "
-import json; d=json.loads(open('$O/r02as_bench_cfg2.json').read()); print(d['value'], d['roofline']['frac'], d['roofline'].get('note','')[:60])"
-python bench.py --workload cfg1 --steps 5 > $O/r02as_bench_cfg1.json 2> $O/r02as_bench_cfg1.err; echo "rc=$?"; python -c "
-import json; d=json.loads(open('$O/r02as_bench_cfg1.json').read()); print(d['value'], d['roofline']['frac'], d['roofline']['l2']['frac'])"
+python bench.py > $O/r02at_bench_default.json 2> $O/r02at_bench_default.err; echo "rc=$?"
+python bench.py --workload cfg1 > $O/r02at_bench_cfg1.json 2> $O/r02at_bench_cfg1.err; echo "rc=$?"
+python bench.py --workload cfg1 --impl reference > $O/r02at_bench_cfg1_reference_arm.json 2> $O/r02at_bench_cfg1_ref.err; echo "rc=$?"
