@@ -46,8 +46,8 @@ WORKLOADS = {
 AESC_WORKLOADS = {
     # name: (graph spec, epsilon, delta, sources per GPU (0 = all), CPU sample sources)
     "cfg3": (("rmat", 16, 8), 0.1, 0.01, 0, 64),
-    "cfg4": (("rmat", 22, 16), 0.05, 0.01, 128, 8),
-    "cfg5": (("chunglu", 3_000_000), 0.01, 0.01, 2048, 64),
+    "cfg4": (("rmat", 22, 16), 0.05, 0.01, 512, 16),
+    "cfg5": (("chunglu", 3_000_000), 0.01, 0.01, 8192, 64),
 }
 BYTES_PER_STEP = 64       # one 32 B sector for {base,deg} + one for adj[base+idx]
 BYTES_PER_EDGE_VISIT = 12  # propagation: 4 B adjacency + 8 B p/d per edge-visit

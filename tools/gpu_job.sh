@@ -1,6 +1,5 @@
-# round-2 GPU job 46: committed bench lines regenerated with the final bench.py (default with the AESC block, cfg1)
+# round-2 GPU job 47: cfg5 (8,192-source subset) and cfg4 (512-source subset, 16 CPU sources) AESC bench lines
 set -x
 O=gpurun_out
-python bench.py > $O/r02at_bench_default.json 2> $O/r02at_bench_default.err; echo "rc=$?"
-python bench.py --workload cfg1 > $O/r02at_bench_cfg1.json 2> $O/r02at_bench_cfg1.err; echo "rc=$?"
-python bench.py --workload cfg1 --impl reference > $O/r02at_bench_cfg1_reference_arm.json 2> $O/r02at_bench_cfg1_ref.err; echo "rc=$?"
+python bench.py --workload cfg5 --warmup 1 --steps 1 > $O/r02au_bench_cfg5.json 2> $O/r02au_bench_cfg5.err; echo "rc=$?"; tail -c 500 $O/r02au_bench_cfg5.json
+python bench.py --workload cfg4 --warmup 1 --steps 1 > $O/r02au_bench_cfg4.json 2> $O/r02au_bench_cfg4.err; echo "rc=$?"; tail -c 500 $O/r02au_bench_cfg4.json
