@@ -222,6 +222,7 @@ def test_campaign_report_names_the_kernel(sb, oracle):
     sink = sb.VisitCountSink(small.n)
     rep = sb.run_walk_campaign(small, sb.CampaignConfig(length=9, master_seed=2), sink, total_walks=20000)
     assert rep.kernel == "walk_count_fat_priv_kernel"
+    assert sb.campaign_tables(small) == (0, small.n)  # every vertex's counter in shared memory
     kv = oracle.uniform_start_counts(small.n, 20000, 2)
     assert np.array_equal(sink.counts, oracle.campaign_counts(small.offsets, small.adjacency, length=9, master=2,
                                                               k_per_vertex=kv))
@@ -232,6 +233,7 @@ def test_campaign_report_names_the_kernel(sb, oracle):
     sinkb = sb.VisitCountSink(big.n)
     repb = sb.run_walk_campaign(big, sb.CampaignConfig(length=17, master_seed=6), sinkb, total_walks=300000)
     assert repb.kernel == "walk_count_rank_kernel"
+    assert sb.campaign_tables(big) == (2560, 22016)  # the 63 KB default split (records, 16-bit counters)
     kvb = oracle.uniform_start_counts(big.n, 300000, 6)
     assert np.array_equal(sinkb.counts, oracle.campaign_counts(big.offsets, big.adjacency, length=17, master=6,
                                                                k_per_vertex=kvb))

@@ -1,5 +1,4 @@
-# round-2 GPU job 47: cfg5 (8,192-source subset) and cfg4 (512-source subset, 16 CPU sources) AESC bench lines
+# round-2 GPU job 48: walk tests after the campaign_tables assertions
 set -x
 O=gpurun_out
-python bench.py --workload cfg5 --warmup 1 --steps 1 > $O/r02au_bench_cfg5.json 2> $O/r02au_bench_cfg5.err; echo "rc=$?"; tail -c 500 $O/r02au_bench_cfg5.json
-python bench.py --workload cfg4 --warmup 1 --steps 1 > $O/r02au_bench_cfg4.json 2> $O/r02au_bench_cfg4.err; echo "rc=$?"; tail -c 500 $O/r02au_bench_cfg4.json
+python -m pytest tests/test_walks_gpu.py -m gpu -x -q -p no:cacheprovider > $O/r02av_pytest.log 2>&1; echo "rc=$?" >> $O/r02av_pytest.log; tail -3 $O/r02av_pytest.log
